@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""MPCD/SRD time-step benchmark (BASELINE.json metric: particle-steps/s and
+fraction of the HBM roofline).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--L 256]
+
+One "step" is one full SRD step (collide + stream + re-bin) of the whole
+workload.  Default workload: BASELINE config 3, a 256^3-cell periodic box at
+10 particles/cell (167,772,160 particles), alpha = 130 deg, dt = 0.1, seed 0,
+the reference's splitmix keyed RNG.  The particle state (17.4 GB with its
+double buffer) is far larger than L2, so no flush is needed between steps.
+
+`value` is timed with CUDA events around K back-to-back steps on the
+engine's stream (state resident in HBM).  `e2e` times the reference-facing
+pure function serial_collision_step through the C ABI (mpcd_step_host) on
+pinned HOST buffers: H2D of positions+velocities, binning, the step, D2H.
+`--impl reference` times the CPU oracle port (oracle/, the reference
+algorithm restated in C, all host threads) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPCD particle-steps/sec"
+UNIT = "particle-steps/s"
+PPC = 10.0
+
+# Algorithmic bytes of one launch, per particle (n) and per cell (C), for the
+# uniform-mass pipeline.
+KERNELS = ("k_collide_count", "k_collide_count_dense", "k_scan", "k_collide_scatter",
+           "k_diag_finalize")
+BYTES_PER_N = {"k_collide_count": 52, "k_collide_count_dense": 0, "k_scan": 0,
+               "k_collide_scatter": 104, "k_diag_finalize": 0}
+BYTES_PER_C = {"k_collide_count": 60, "k_collide_count_dense": 0, "k_scan": 12,
+               "k_collide_scatter": 60, "k_diag_finalize": 64.0 / 32}
+SURVEY_B_ALG_N, SURVEY_B_ALG_C = 216, 28  # B_alg = 216 n + 28 C
+B_MIN_N = 96                              # compulsory: read + write x, v once
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--L", type=int, default=256, help="cells per box edge (per GPU)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-L", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+        return False
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(L, steps, seed):
+    """The oracle (reference algorithm restated in C) on a bounded sample."""
+    import numpy as np
+
+    import oracle
+
+    threads = oracle.set_threads(os.cpu_count() or 1)
+    pos, vel, mass = oracle.init_system(L, PPC, seed)
+    cs, sn = float(np.cos(np.radians(130.0))), float(np.sin(np.radians(130.0)))
+    oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, seed, 0)  # warm-up
+    t0 = time.perf_counter()
+    for k in range(1, steps + 1):
+        r = oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, seed, k)
+        pos, vel = r.positions, r.velocities
+    dt = time.perf_counter() - t0
+    n = pos.shape[0]
+    return {"value": n * steps / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle/mpcd_oracle.c serial step, {L}^3 cells x {PPC:g} ({n} particles), "
+                      f"{steps} steps after 1 warm-up, {threads} OpenMP threads, "
+                      f"{dt / steps:.3f} s/step"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    L = args.cpu_sample_L
+    import numpy as np
+
+    import oracle
+
+    threads = oracle.set_threads(os.cpu_count() or 1)
+    pos, vel, mass = oracle.init_system(L, PPC, args.seed)
+    n = pos.shape[0]
+    cs, sn = float(np.cos(np.radians(130.0))), float(np.sin(np.radians(130.0)))
+    for k in range(args.warmup):
+        r = oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, args.seed, k)
+        pos, vel = r.positions, r.velocities
+    t0 = time.perf_counter()
+    for k in range(args.warmup, args.warmup + args.steps):
+        r = oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, args.seed, k)
+        pos, vel = r.positions, r.velocities
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle init_system)",
+        "config": {"workload": f"{args.L}^3 cells x 10 particles/cell periodic SRD box, 130 deg, "
+                               f"dt 0.1, seed {args.seed} (timed on a {L}^3 sample)",
+                   "cells": L ** 3, "particles": n, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{L}^3 cells x 10 ({n} particles) per step, "
+                                   f"{threads} OpenMP threads; the reference package is pure "
+                                   "Python/numpy and is not installed on the GPU box, so its "
+                                   "bit-exact C restatement (oracle/) is timed"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    ws, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2212_11878_b200 import _lib
+    from paper_2212_11878_b200.engine import EngineContext
+    from paper_2212_11878_b200.params import SimParams
+
+    L = args.L
+    params = SimParams(edge_length=L, seed=args.seed + rank)
+    n = params.n_particles
+    C = params.n_cells
+    ctx = EngineContext(params.dims, params.cell_size, params.dt, params.alpha, params.seed,
+                        params.prng, n, mass_value=1.0)
+    ctx.init_device(n, 1.0, 0)
+    stream = torch.cuda.current_stream()
+    ctx.run(0, args.warmup)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        start.record(stream)
+        ctx.run(args.warmup, args.steps)
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = start.elapsed_time(end) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * n / (ms * 1e-3)
+    d = ctx.read_diag()
+
+    # per-kernel timing (CUDA events on the engine stream), separate pass
+    import ctypes as C_
+    lib = _lib.load()
+    lib.mpcd_profile(ctx.handle, 1)
+    prof_steps = max(3, min(args.steps, 10))
+    ctx.run(args.warmup + args.steps, prof_steps)
+    kms = (C_.c_double * 5)()
+    nst = C_.c_int64(0)
+    _lib.check(lib.mpcd_read_profile(ctx.handle, kms, C_.byref(nst)))
+    lib.mpcd_profile(ctx.handle, 0)
+    per_kernel = {k: kms[i] / max(nst.value, 1) for i, k in enumerate(KERNELS)}
+    top = max(per_kernel, key=per_kernel.get)
+    alg = {k: BYTES_PER_N[k] * n + BYTES_PER_C[k] * C for k in KERNELS}
+    peak, peak_src = peaks()
+    achieved = alg[top] / (per_kernel[top] * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                tr = json.load(f)
+            if tr.get("L") == L and top in tr.get("kernels", {}):
+                traffic = tr["kernels"][top]
+        except Exception:
+            traffic = None
+    step_bytes = sum(alg.values())
+    survey_bytes = SURVEY_B_ALG_N * n + SURVEY_B_ALG_C * C
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device init_system: uniform positions, N(0,1) velocities minus "
+                "their mean, unit masses)",
+        "config": {"workload": f"{L}^3 cells x 10 particles/cell periodic SRD box per GPU "
+                               f"(BASELINE config {'3' if L == 256 else 'custom'}), 130 deg, "
+                               "dt 0.1, splitmix keyed RNG",
+                   "cells_per_gpu": C, "particles_per_gpu": n,
+                   "parallelism": "single domain" if ws == 1 else
+                   f"replicas x{ws} (independent periodic boxes, seed + rank)",
+                   "l2": "state 17 GB >> 126 MB L2; no flush needed"},
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg[top],
+                     "avg_launch_ms": per_kernel[top], "peak_source": peak_src},
+        "roofline_step": {
+            "bytes_per_step": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9,
+            "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+            "survey_b_alg_frac": survey_bytes / (ms * 1e-3) / 1e9 / peak,
+            "b_min_frac": B_MIN_N * n / (ms * 1e-3) / 1e9 / peak,
+            "kernel_ms": per_kernel},
+        "gpu_launches": args.steps * 5,
+        "diag_last": {"momentum": list(d.momentum), "energy": d.energy, "mass": d.mass},
+    }
+    line["clocks"] = clocks.summary()
+    if rank == 0 and not args.no_e2e:
+        line["e2e"], line["e2e_stateful"] = e2e(args, params, ctx)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_sample_L, 3, args.seed)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e(args, params, ctx):
+    """Pure-function step through the C ABI on pinned host buffers, and the
+    stateful Simulation-style step with its per-step diagnostics read-back."""
+    import numpy as np
+    import torch
+
+    n = params.n_particles
+    pos_t = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+    vel_t = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+    pos, vel = pos_t.numpy(), vel_t.numpy()
+    ids, p = ctx.download(id_order=True)
+    pos[:] = p.positions
+    vel[:] = p.velocities
+    del p, ids
+    step0 = 1000
+    ctx.step_host(pos, vel, None, step0, False)  # warm-up
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    K = args.e2e_steps
+    s.record()
+    for k in range(K):
+        ctx.step_host(pos, vel, None, step0 + 1 + k, False)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) * 1e-3
+    pure = {"value": n * K / t, "unit": UNIT, "h2d_bytes_per_step": 48 * n,
+            "d2h_bytes_per_step": 48 * n + 64,
+            "api": "mpcd_step_host == serial_collision_step(ParticleSet, params, step) on "
+                   "pinned host (n,3) float64 arrays"}
+    # stateful: Simulation.step() == mpcd_step + mpcd_read_diag (64 B D2H)
+    ctx.upload(pos, vel, None, None, step0 + K + 1)
+    torch.cuda.synchronize()
+    s.record()
+    for k in range(args.steps):
+        ctx.step(step0 + K + 1 + k)
+        ctx.read_diag()
+    e.record()
+    torch.cuda.synchronize()
+    t2 = s.elapsed_time(e) * 1e-3
+    stateful = {"value": n * args.steps / t2, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 64, "api": "Simulation.step() (state resident, "
+                                                 "diagnostics read back every step)"}
+    return pure, stateful
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

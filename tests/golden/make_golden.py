@@ -156,6 +156,7 @@ def _run_serial(params, p0, steps, tag, out):
     out[f"{tag}_a"] = np.float64(params.cell_size)
     out[f"{tag}_cos"] = np.float64(np.cos(params.alpha))
     out[f"{tag}_sin"] = np.float64(np.sin(params.alpha))
+    out[f"{tag}_alpha"] = np.float64(params.alpha)
     out[f"{tag}_steps"] = np.int64(steps)
     out[f"{tag}_pos0"], out[f"{tag}_vel0"], out[f"{tag}_mass"] = p.positions, p.velocities, p.masses
     for k in range(steps):

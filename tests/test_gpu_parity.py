@@ -1,0 +1,303 @@
+"""GPU parity: every stage and the full step vs the reference's golden
+vectors (bit-exact) and vs the CPU oracle on seeded inputs.
+
+Run on a B200: python -m pytest tests -m gpu
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2212_11878_b200 as mp
+from paper_2212_11878_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+# ---------------------------------------------------------------- stages ---
+def test_grid_shift_and_axes_match_reference(g_rng):
+    for seed, rows in zip(g_rng["shift_seeds"], g_rng["shifts"]):
+        got = np.array([mp.sample_grid_shift(s, int(seed)).offset for s in range(rows.shape[0])])
+        assert np.array_equal(got, rows)
+    got = np.array([mp.sample_grid_shift(s, 9, 2.5).offset for s in range(50)])
+    assert np.array_equal(got, g_rng["shifts_a25"])
+    assert np.array_equal(mp.sample_rotation_axes(7, g_rng["axes_ids"], 42), g_rng["axes"])
+    assert np.array_equal(mp.sample_rotation_axes(5, g_rng["axes_sparse_ids"], 11),
+                          g_rng["axes_sparse"])
+    su = mp.sample_uniform(mp.RngKey(seed=42, step=7, purpose=mp.Purpose.AXIS, cell_id=123), 64)
+    assert np.array_equal(su, g_rng["sample_uniform"])
+
+
+@pytest.mark.parametrize("kind", ["minstd", "pcg32", "sfc64"])
+def test_keyed_prng_streams_match_oracle(kind):
+    key = mp.RngKey(seed=42, step=3, purpose=mp.Purpose.AXIS, cell_id=77)
+    got = mp.sample_uniform(key, 1000, prng=kind)
+    want = oracle.sample_uniform(kind, 42, 3, oracle.AXIS, 77, 1000)
+    assert np.array_equal(got, want)
+    ids = np.arange(5000)
+    assert np.array_equal(mp.sample_rotation_axes(9, ids, 42, prng=kind),
+                          oracle.rotation_axes(9, ids, 42, prng=kind))
+    for s in range(20):
+        assert np.array_equal(mp.sample_grid_shift(s, 42, 1.0, kind).offset,
+                              oracle.grid_shift(s, 42, 1.0, kind))
+
+
+@pytest.mark.parametrize("case", list("ABCDEF"))
+def test_binning_and_moments_match_reference(g_collision, case):
+    g = g_collision
+    dims = g[f"{case}_dims"]
+    a = float(g[f"{case}_a"])
+    gmin = g[f"{case}_gmin"]
+    lc = mp.build_linked_cells(g[f"{case}_pos"], a, gmin, gmin + dims * a, wrap=g[f"{case}_wrap"])
+    assert np.array_equal(lc.cells, g[f"{case}_cells"])
+    assert np.array_equal(lc.bin_count, g[f"{case}_counts"])
+    assert np.array_equal(lc.bin_offset, g[f"{case}_offsets"])
+    assert np.array_equal(lc.permutation, g[f"{case}_perm"])
+    mom = mp.segment_moments(lc, g[f"{case}_vel"], g[f"{case}_mass"])
+    assert np.array_equal(mom, g[f"{case}_moments"])
+    assert np.array_equal(mp.finalize_com(mp.CellMomentField(mom)), g[f"{case}_com"])
+    alt = mp.linked_cells_from_indices(lc.cells, dims, gmin, gmin + dims * a, a, lc.wrap)
+    assert np.array_equal(alt.permutation, lc.permutation)
+
+
+def test_binning_error_matches_reference(g_collision):
+    with pytest.raises(mp.BinningError) as info:
+        mp.build_linked_cells(g_collision["err_pos"], 1.0, np.zeros(3), np.full(3, 2.0))
+    assert [info.value.particle_index, info.value.dimension] == list(g_collision["err_info"])
+    with pytest.raises(mp.BinningError):
+        mp.linked_cells_from_indices(np.array([0, 8]), (2, 2, 2), np.zeros(3), np.full(3, 2.0),
+                                     1.0, (False,) * 3)
+
+
+@pytest.mark.parametrize("tag", ["r1", "r130", "rq"])
+def test_rotation_matches_reference(g_collision, tag):
+    g = g_collision
+    got = mp.rotate_velocities(g["rot_vel"], g["rot_com"], g["rot_axes"], float(g[f"{tag}_alpha"]))
+    assert np.array_equal(got, g[f"{tag}_out"])
+
+
+def test_wrap_and_stream_match_reference(g_collision):
+    g = g_collision
+    got = mp.wrap_coordinates(g["wrap_x"], 8.0)
+    assert np.array_equal(got, g["wrap_out"])
+    assert np.array_equal(np.signbit(got), np.signbit(g["wrap_out"]))
+    p = mp.ParticleSet(g["stream_pos"], g["stream_vel"], np.ones(3000))
+    assert np.array_equal(mp.stream_and_wrap(p, 0.7, 8.0).positions, g["stream_out"])
+
+
+def test_drift_metric_values():
+    before = np.array([[1.0, 0.0, 0.0, 2.0], [0.0, 0.0, 0.0, 0.0]])
+    assert mp.cell_momentum_drift(before, before) == 0.0
+    bumped = before.copy()
+    bumped[0, 0] += 0.5
+    assert mp.cell_momentum_drift(before, bumped) == pytest.approx(0.25)
+    assert mp.cell_momentum_drift(np.zeros((4, 4)), np.zeros((4, 4))) == 0.0
+
+
+# -------------------------------------------------------- the full step ---
+@pytest.mark.parametrize("tag", ["L4", "L6", "M4", "B5"])
+def test_pure_step_matches_reference(g_serial, tag):
+    """serial_collision_step (GPU) == reference, every intermediate, bitwise."""
+    g = g_serial
+    params = mp.SimParams(edge_length=int(g[f"{tag}_L"]), seed=int(g[f"{tag}_seed"]),
+                          dt=float(g[f"{tag}_dt"]), alpha=float(g[f"{tag}_alpha"]))
+    assert float(np.cos(params.alpha)) == float(g[f"{tag}_cos"])
+    p = mp.ParticleSet(g[f"{tag}_pos0"], g[f"{tag}_vel0"], g[f"{tag}_mass"])
+    for k in range(int(g[f"{tag}_steps"])):
+        p, drift, (occ, com) = mp.serial_collision_step(p, params, k, want_drift=True,
+                                                        want_com=True)
+        assert np.array_equal(p.positions, g[f"{tag}_pos{k + 1}"]), k
+        assert np.array_equal(p.velocities, g[f"{tag}_vel{k + 1}"]), k
+        assert np.array_equal(occ, g[f"{tag}_occ{k}"])
+        assert np.array_equal(com, g[f"{tag}_com{k}"])
+        assert drift == pytest.approx(float(g[f"{tag}_drift{k}"]), rel=1e-6, abs=1e-15)
+
+
+def _sim_from_state(params, pos, vel, **kw):
+    sim = mp.Simulation(params, backend="cuda", **kw)
+    sim.runner.ctx.upload(pos, vel, None, None, 0)
+    return sim
+
+
+def test_config1_engine_100_steps_bitexact(g_config1):
+    """BASELINE config 1 through the resident engine: binning (cells, counts,
+    permutation) and state hashes equal the reference at every step."""
+    g = g_config1
+    params = mp.SimParams(edge_length=16, seed=int(g["seed"]), dt=float(g["dt"]))
+    assert float(np.cos(params.alpha)) == float(g["cos"])
+    sim = _sim_from_state(params, g["pos0"], g["vel0"], capture_drift=True)
+    ctx = sim.runner.ctx
+    try:
+        for k in range(int(g["steps"])):
+            cells, counts, offsets, perm = ctx.read_binning()
+            assert sha(cells, counts, perm) == str(g["bin_sha"][k]), k
+            d = sim.step()
+            ids, p = sim.collect()
+            assert np.array_equal(ids, np.arange(p.n))
+            assert sha(p.positions, p.velocities) == str(g["state_sha"][k]), k
+            ref = g["diag"][k]
+            assert np.allclose(d["momentum"], ref[:3], atol=1e-10)
+            assert d["energy"] == pytest.approx(ref[3], rel=1e-12)
+            assert d["mass"] == ref[4]
+            assert d["max_cell_drift"] == pytest.approx(ref[5], rel=1e-3, abs=1e-15)
+        assert np.array_equal(p.positions, g["pos_final"])
+    finally:
+        sim.close()
+
+
+def test_host_init_matches_reference(g_config1):
+    p = mp.init_system(mp.SimParams(edge_length=16, seed=42))
+    assert sha(p.positions, p.velocities) == str(g_config1["init_sha"])
+
+
+def _oracle_run(pos, vel, mass, dims, params, steps, start=0):
+    cs, sn = float(np.cos(params.alpha)), float(np.sin(params.alpha))
+    for k in range(start, start + steps):
+        r = oracle.serial_step(pos, vel, mass, dims, params.cell_size, params.dt, cs, sn,
+                               params.seed, k, prng=params.prng)
+        pos, vel = r.positions, r.velocities
+    return pos, vel
+
+
+@pytest.mark.parametrize("prng", ["splitmix", "minstd", "pcg32", "sfc64"])
+def test_engine_64cubed_matches_oracle(prng):
+    """Config 2: 64^3 x 10 (2.6M particles), each PRNG, 4 steps bitwise."""
+    params = mp.SimParams(edge_length=64, seed=1, prng=prng)
+    sim = mp.Simulation(params, backend="cuda", init="device")
+    try:
+        ids, p0 = sim.collect()
+        sim.run(4)
+        ids, p = sim.collect()
+    finally:
+        sim.close()
+    pos, vel = _oracle_run(p0.positions, p0.velocities, np.ones(p0.n), 64, params, 4)
+    assert np.array_equal(p.positions, pos)
+    assert np.array_equal(p.velocities, vel)
+
+
+def test_config2_reference_hashes():
+    """64^3 seed 0 against the reference's own trajectory hashes."""
+    from conftest import golden
+    g = golden("config2_L64.npz")
+    params = mp.SimParams(edge_length=64, seed=0)
+    p = mp.init_system(params)
+    if sha(p.positions, p.velocities) != str(g["init_sha"]):
+        pytest.skip("host numpy transcendental results differ from the fixture host")
+    sim = _sim_from_state(params, p.positions, p.velocities)
+    try:
+        for k in range(int(g["steps"])):
+            cells, counts, offsets, perm = sim.runner.ctx.read_binning()
+            assert sha(cells, counts, perm) == str(g["bin_sha"][k])
+            sim.step()
+            _, q = sim.collect()
+            assert sha(q.positions, q.velocities) == str(g["state_sha"][k])
+    finally:
+        sim.close()
+
+
+def test_noncubic_box_matches_oracle():
+    params = mp.SimParams(edge_length=24, edge_lengths=(24, 16, 8), seed=5)
+    sim = mp.Simulation(params, backend="cuda")
+    try:
+        _, p0 = sim.collect()
+        sim.run(5)
+        _, p = sim.collect()
+    finally:
+        sim.close()
+    pos, vel = _oracle_run(p0.positions, p0.velocities, np.ones(p0.n), [24, 16, 8], params, 5)
+    assert np.array_equal(p.positions, pos) and np.array_equal(p.velocities, vel)
+
+
+def test_dense_cells_overflow_path():
+    """Tiles far above the shared-memory capacity (clustered particles)."""
+    rs = np.random.default_rng(3)
+    n = 6000
+    pos = np.concatenate([rs.uniform(2.0, 2.9, size=(5000, 3)), rs.uniform(0, 8, size=(1000, 3))])
+    vel = rs.normal(size=(n, 3))
+    params = mp.SimParams(edge_length=8, seed=9, mean_density=n / 512)
+    p = mp.ParticleSet(pos, vel, np.ones(n))
+    ref_pos, ref_vel = pos, vel
+    for k in range(4):
+        p, drift, _ = mp.serial_collision_step(p, params, k, want_drift=True)
+        ref_pos, ref_vel = _oracle_run(ref_pos, ref_vel, np.ones(n), 8, params, 1, start=k)
+        assert np.array_equal(p.positions, ref_pos) and np.array_equal(p.velocities, ref_vel), k
+        assert drift < 1e-12
+
+
+def test_empty_and_tiny_systems():
+    params = mp.SimParams(edge_length=4, seed=1)
+    p = mp.ParticleSet.empty()
+    out, drift, com = mp.serial_collision_step(p, params, 0, want_drift=True, want_com=True)
+    assert out.n == 0 and drift == 0.0 and com[0].size == 0
+    one = mp.ParticleSet(np.array([[0.5, 1.5, 3.99]]), np.array([[1.0, -2.0, 0.5]]), np.ones(1))
+    out, _, _ = mp.serial_collision_step(one, params, 3)
+    ref_pos, ref_vel = _oracle_run(one.positions, one.velocities, np.ones(1), 4, params, 1, 3)
+    assert np.array_equal(out.positions, ref_pos) and np.array_equal(out.velocities, ref_vel)
+
+
+def test_conservation_and_determinism():
+    params = mp.SimParams(edge_length=16, seed=3)
+    a = mp.Simulation(params, backend="cuda", capture_drift=True)
+    b = mp.Simulation(params, backend="cuda", capture_drift=True)
+    try:
+        r0 = a.conservation_report()
+        a.run(50)
+        b.run(50)
+        r1 = a.conservation_report()
+        assert r1.n_particles == r0.n_particles and r1.total_mass == r0.total_mass
+        assert np.abs(r1.total_momentum - r0.total_momentum).max() < 1e-10
+        assert abs(r1.kinetic_energy - r0.kinetic_energy) < 1e-9 * r0.kinetic_energy
+        assert max(a.drift_history) < 1e-10
+        ia, pa = a.collect()
+        ib, pb = b.collect()
+        assert np.array_equal(pa.positions, pb.positions)
+        assert np.array_equal(pa.velocities, pb.velocities)
+        assert [d["momentum"].tobytes() for d in a.diagnostics] == \
+               [d["momentum"].tobytes() for d in b.diagnostics]
+    finally:
+        a.close()
+        b.close()
+
+
+def test_galilean_boost():
+    """Acceptance criterion 8 (test_acceptance.py:251-268) on the GPU step."""
+    w = np.array([1.0, 2.0, 3.0])
+    params = mp.SimParams(edge_length=8, dt=8.0, seed=3)
+    base = mp.init_system(params)
+    boosted = mp.ParticleSet(base.positions.copy(), base.velocities + w, base.masses.copy())
+    for step in range(20):
+        base, _, _ = mp.serial_collision_step(base, params, step)
+        boosted, _, _ = mp.serial_collision_step(boosted, params, step)
+    assert np.abs(boosted.velocities - w - base.velocities).max() < 1e-9
+
+
+def test_advance_equals_step_loop():
+    params = mp.SimParams(edge_length=12, seed=8)
+    a = mp.Simulation(params, backend="cuda")
+    b = mp.Simulation(params, backend="cuda")
+    try:
+        a.run(7)
+        b.advance(7)
+        _, pa = a.collect()
+        _, pb = b.collect()
+        assert np.array_equal(pa.positions, pb.positions)
+        assert np.array_equal(pa.velocities, pb.velocities)
+    finally:
+        a.close()
+        b.close()
