@@ -35,14 +35,15 @@ METRIC = "MPCD particle-steps/sec"
 UNIT = "particle-steps/s"
 PPC = 10.0
 
-# Algorithmic bytes of one launch, per particle (n) and per cell (C), for the
-# uniform-mass pipeline.
-KERNELS = ("k_collide_count", "k_collide_count_dense", "k_scan", "k_collide_scatter",
-           "k_diag_finalize")
-BYTES_PER_N = {"k_collide_count": 52, "k_collide_count_dense": 0, "k_scan": 0,
-               "k_collide_scatter": 104, "k_diag_finalize": 0}
-BYTES_PER_C = {"k_collide_count": 60, "k_collide_count_dense": 0, "k_scan": 12,
-               "k_collide_scatter": 60, "k_diag_finalize": 64.0 / 32}
+# Algorithmic bytes of one launch, per particle (n) and per cell (C)
+# (DESIGN.md section 3).  A particle is two 32-byte records; k_step reads
+# each once from its cell region and writes it once into its next-step cell;
+# per cell it reads + zeroes this step's count, updates the next count
+# (atomic, 8) and writes 64 B of partials per 32-cell tile.
+KERNELS = ("k_step", "k_step_dense", "k_diag")  # mpcd_read_profile slots 0..2
+LAUNCHES_PER_STEP = 4  # k_step, k_step_dense, k_diag_partial, k_diag_finalize
+BYTES_PER_N = {"k_step": 128, "k_step_dense": 0, "k_diag": 0}
+BYTES_PER_C = {"k_step": 16 + 64.0 / 32, "k_step_dense": 0, "k_diag": 64.0 / 32}
 SURVEY_B_ALG_N, SURVEY_B_ALG_C = 216, 28  # B_alg = 216 n + 28 C
 B_MIN_N = 96                              # compulsory: read + write x, v once
 
@@ -286,7 +287,7 @@ def run_ours(args):
             "survey_b_alg_frac": survey_bytes / (ms * 1e-3) / 1e9 / peak,
             "b_min_frac": B_MIN_N * n / (ms * 1e-3) / 1e9 / peak,
             "kernel_ms": per_kernel},
-        "gpu_launches": args.steps * 5,
+        "gpu_launches": args.steps * LAUNCHES_PER_STEP,
         "diag_last": {"momentum": list(d.momentum), "energy": d.energy, "mass": d.mass},
     }
     line["clocks"] = clocks.summary()

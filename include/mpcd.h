@@ -108,6 +108,8 @@ int mpcd_download(mpcd_ctx* ctx, double* pos, double* vel, double* mass, int64_t
                   int32_t id_order, void* stream);
 
 int64_t mpcd_count(const mpcd_ctx* ctx);
+/* Record slots per cell region (fixed-capacity cell layout). */
+int64_t mpcd_cell_capacity(const mpcd_ctx* ctx);
 int64_t mpcd_current_step(const mpcd_ctx* ctx);
 
 /* One collision + streaming step with index `step` (the reference's
@@ -148,7 +150,8 @@ int mpcd_init_device(mpcd_ctx* ctx, int64_t n, double velocity_variance, int64_t
 /* Per-kernel CUDA-event timing of subsequent mpcd_step/mpcd_run calls
  * (enable=0 stops and clears).  mpcd_read_profile synchronises and returns
  * the summed milliseconds per kernel slot, MPCD_PROFILE_SLOTS entries:
- * collide_count, collide_count_dense, scan, collide_scatter, diag_finalize. */
+ * [0] k_step (the tile kernel), [1] k_step_dense, [2] diagnostics
+ * reduction (k_diag_partial + k_diag_finalize), [3], [4] reserved (0). */
 #define MPCD_PROFILE_SLOTS 5
 int mpcd_profile(mpcd_ctx* ctx, int32_t enable);
 int mpcd_read_profile(mpcd_ctx* ctx, double* ms, int64_t* n_steps);

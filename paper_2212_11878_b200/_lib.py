@@ -62,6 +62,7 @@ SIGNATURES = {
     "mpcd_upload": (C.c_int, [_vp, _d, _d, _d, _i64, C.c_int64, C.c_int64, _vp]),
     "mpcd_download": (C.c_int, [_vp, _d, _d, _d, _i64, C.c_int32, _vp]),
     "mpcd_count": (C.c_int64, [_vp]),
+    "mpcd_cell_capacity": (C.c_int64, [_vp]),
     "mpcd_current_step": (C.c_int64, [_vp]),
     "mpcd_step": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp]),
     "mpcd_run": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int32, _vp]),

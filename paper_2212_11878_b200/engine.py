@@ -143,7 +143,8 @@ class EngineContext:
             offsets.ctypes.data_as(_lib._i64), perm.ctypes.data_as(_lib._i64), _dev.stream()))
         return cells, counts, offsets, perm
 
-    def step_host(self, positions, velocities, masses, step: int, want_drift: bool):
+    def step_host(self, positions, velocities, masses, step: int, want_drift: bool,
+                  want_com: bool = False):
         """serial_collision_step on host buffers (overwritten in place)."""
         n = positions.shape[0]
         drift = C.c_double(0.0)
@@ -151,7 +152,8 @@ class EngineContext:
         _lib.check(self._lib.mpcd_step_host(
             self.handle, positions.ctypes.data_as(_lib._d), velocities.ctypes.data_as(_lib._d),
             m.ctypes.data_as(_lib._d) if m is not None else None, n, int(step),
-            _lib.STEP_WANT_DRIFT if want_drift else 0, C.byref(drift), _dev.stream()))
+            (_lib.STEP_WANT_DRIFT if want_drift else 0) | (_lib.STEP_WANT_COM if want_com else 0),
+            C.byref(drift), _dev.stream()))
         return drift.value
 
 
@@ -193,7 +195,7 @@ def serial_collision_step(p: ParticleSet, params: SimParams, step: int, *,
     vel = np.array(p.velocities, dtype=np.float64, order="C", copy=True)
     masses = np.ascontiguousarray(p.masses, dtype=np.float64)
     ctx = _context_for(params, p.n, _uniform_mass(masses))
-    drift = ctx.step_host(pos, vel, masses, step, want_drift)
+    drift = ctx.step_host(pos, vel, masses, step, want_drift, want_com)
     com = ctx.read_com() if want_com else None
     return ParticleSet(pos, vel, p.masses), (drift if want_drift else None), com
 
@@ -242,7 +244,8 @@ class CudaRunner:
         self._last = None
 
     def run_step(self, step: int) -> dict:
-        flags = _lib.STEP_WANT_DRIFT if self.capture_drift else 0
+        flags = (_lib.STEP_WANT_DRIFT if self.capture_drift else 0) | \
+            (_lib.STEP_WANT_COM if self.capture_com else 0)
         self.ctx.step(step, flags)
         d = self.ctx.read_diag()
         self._last = d
