@@ -21,6 +21,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "mpcd_internal.h"
@@ -430,18 +433,47 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.step = (uint64_t)step;
   A.prng = g.prng;
   A.m0 = g.mass_value;
+  A.part_base = 0;
   (void)by_id;
   return A;
 }
 
-// which == 0: the tile kernel; which == 1: the dense-tile kernel
+// Resident CTAs per device for a persistent kernel, cached per (kernel, device).
+int64_t resident_ctas(const void* kernel, int block, size_t smem) {
+  static std::map<std::pair<const void*, int>, int64_t> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto key = std::make_pair(kernel, dev);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    it = cache.emplace(key, (int64_t)std::max(per_sm, 1) * sms).first;
+  }
+  return it->second;
+}
+
+constexpr int64_t kDenseGrid = 592;
+
+// which == 0: the persistent tile kernel (returns its grid); which == 1: the
+// dense-tile kernel after sorting its tile list.
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
-void launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_t st) {
-  if (which == 0)
-    k_step<UNIT, UMASS, DRIFT, COM, BYID><<<(unsigned)ntiles, kNT, 0, st>>>(A);
-  else
-    k_step_dense<UNIT, UMASS, DRIFT, COM, BYID>
-        <<<(unsigned)std::min<int64_t>(ntiles, 592), kNT, 0, st>>>(A);
+int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_t st) {
+  if (which == 0) {
+    auto kern = k_step<UNIT, UMASS, DRIFT, COM, BYID>;
+    const size_t smem = sizeof(StepSmem<DRIFT>);
+    const int64_t grid =
+        std::max<int64_t>(1, std::min<int64_t>(ntiles, resident_ctas((const void*)kern, kNTW, smem)));
+    kern<<<(unsigned)grid, kNTW, smem, st>>>(A, ntiles);
+    return grid;
+  }
+  k_sort_dense<<<1, 1, 0, st>>>(A.dense, A.flags);
+  k_step_dense<UNIT, UMASS, DRIFT, COM, BYID><<<(unsigned)kDenseGrid, kNT, 0, st>>>(A);
+  return kDenseGrid;
 }
 
 // 32 compile-time variants, chosen at run time
@@ -449,28 +481,27 @@ struct Variant {
   bool unit, umass, drift, com, by_id;
 };
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM>
-void launch_byid(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.by_id) launch_variant<UNIT, UMASS, DRIFT, COM, true>(A, nt, which, st);
-  else launch_variant<UNIT, UMASS, DRIFT, COM, false>(A, nt, which, st);
+int64_t launch_byid(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
+  if (v.by_id) return launch_variant<UNIT, UMASS, DRIFT, COM, true>(A, nt, which, st);
+  return launch_variant<UNIT, UMASS, DRIFT, COM, false>(A, nt, which, st);
 }
 template <bool UNIT, bool UMASS, bool DRIFT>
-void launch_com(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.com) launch_byid<UNIT, UMASS, DRIFT, true>(A, nt, v, which, st);
-  else launch_byid<UNIT, UMASS, DRIFT, false>(A, nt, v, which, st);
+int64_t launch_com(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
+  if (v.com) return launch_byid<UNIT, UMASS, DRIFT, true>(A, nt, v, which, st);
+  return launch_byid<UNIT, UMASS, DRIFT, false>(A, nt, v, which, st);
 }
 template <bool UNIT, bool UMASS>
-void launch_drift(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.drift) launch_com<UNIT, UMASS, true>(A, nt, v, which, st);
-  else launch_com<UNIT, UMASS, false>(A, nt, v, which, st);
+int64_t launch_drift(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
+  if (v.drift) return launch_com<UNIT, UMASS, true>(A, nt, v, which, st);
+  return launch_com<UNIT, UMASS, false>(A, nt, v, which, st);
 }
-void launch_step_kernel(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
+int64_t launch_step_kernel(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
   if (v.unit) {
-    if (v.umass) launch_drift<true, true>(A, nt, v, which, st);
-    else launch_drift<true, false>(A, nt, v, which, st);
-  } else {
-    if (v.umass) launch_drift<false, true>(A, nt, v, which, st);
-    else launch_drift<false, false>(A, nt, v, which, st);
+    if (v.umass) return launch_drift<true, true>(A, nt, v, which, st);
+    return launch_drift<true, false>(A, nt, v, which, st);
   }
+  if (v.umass) return launch_drift<false, true>(A, nt, v, which, st);
+  return launch_drift<false, false>(A, nt, v, which, st);
 }
 
 int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t st) {
@@ -489,13 +520,14 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
   }
   const Variant v{c->cfg.cell_size == 1.0, c->cfg.uniform_mass != 0,
                   (flags & MPCD_STEP_WANT_DRIFT) != 0, com, by_id};
-  launch_step_kernel(A, c->ntiles, v, 0, st);
+  const int64_t grid = launch_step_kernel(A, c->ntiles, v, 0, st);
   MPCD_LAUNCH_CHECK();
   if (ev) MPCD_CUDA(cudaEventRecord(ev[1], st));
-  launch_step_kernel(A, c->ntiles, v, 1, st);
+  A.part_base = grid;  // the dense CTAs' partial rows follow the tile kernel's
+  const int64_t nparts = grid + launch_step_kernel(A, c->ntiles, v, 1, st);
   MPCD_LAUNCH_CHECK();
   if (ev) MPCD_CUDA(cudaEventRecord(ev[2], st));
-  k_diag_partial<<<kDiagBlocks, 256, 0, st>>>(c->partials, c->ntiles, c->level1);
+  k_diag_partial<<<kDiagBlocks, 256, 0, st>>>(c->partials, nparts, c->level1);
   MPCD_LAUNCH_CHECK();
   k_diag_finalize<<<1, 32, 0, st>>>(c->level1, kDiagBlocks, c->drift_bits, c->diag, c->n, step,
                                     flags_of(c), ovf_n_of(c, c->cur), scratch_n_of(c));
@@ -566,7 +598,7 @@ int mpcd_ctx_create(const mpcd_config* cfg, mpcd_ctx** out) {
       cudaMalloc(&c->scratch_id, sizeof(uint32_t) * c->scratch_cap) != cudaSuccess ||
       cudaMalloc(&c->scratch_src, sizeof(uint32_t) * c->scratch_cap) != cudaSuccess ||
       cudaMalloc(&c->scratch_val, sizeof(double) * 4 * c->scratch_cap) != cudaSuccess ||
-      cudaMalloc(&c->partials, sizeof(double) * 8 * c->ntiles) != cudaSuccess ||
+      cudaMalloc(&c->partials, sizeof(double) * 8 * (c->ntiles + kDenseGrid)) != cudaSuccess ||
       cudaMalloc(&c->level1, sizeof(double) * 5 * kDiagBlocks) != cudaSuccess ||
       cudaMalloc(&c->diag, sizeof(double) * 8) != cudaSuccess ||
       cudaMalloc(&c->drift_bits, sizeof(unsigned long long)) != cudaSuccess)

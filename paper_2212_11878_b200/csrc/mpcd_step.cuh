@@ -84,6 +84,7 @@ struct StepArgs {
   uint64_t seed, step;
   int prng;
   double m0;
+  int64_t part_base;          // first partials row of the dense kernel's CTAs
 };
 
 constexpr int kTC = 32;         // cells per tile (one warp owns the per-cell work)
@@ -225,227 +226,368 @@ __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, 
   if (active) finish_slot(A, key, grp, base, o, id, m);
 }
 
-// ------------------------------------------------------- the step kernel --
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
-__global__ void __launch_bounds__(kNT, 3) k_step(const StepArgs A) {
-  __shared__ uint32_t s_cnt[kTC];
-  __shared__ uint32_t s_off[kTC + 1];  // padded (multiple-of-4) segment starts
-  __shared__ __align__(16) uint32_t s_id[kMaxP];
-  __shared__ uint8_t s_cell[kMaxP];
-  __shared__ __align__(16) double s_val[kMaxP * 4];
-  __shared__ double s_mom[kTC * 4];
-  __shared__ double s_post[DRIFT ? kTC * 4 : 1];
-  __shared__ double s_cx[kTC * 6];
-  __shared__ double s_red[(kNT / 32) * 4];
-  __shared__ int s_dense;
-  const int t = threadIdx.x, lane = t & 31;
-  const int64_t tile = blockIdx.x;
-  const int64_t c0 = tile * kTC;
-  const int nc = (int)min((int64_t)kTC, A.C - c0);
+// ------------------------------------------------------------ TMA helpers --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MPCD_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MPCD_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 1-D bulk copy global -> shared (TMA), completion counted on `bar`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 
-  // phase 0 (warp 0): counts, padded segment offsets, dense-tile test
-  if (t < 32) {
-    const uint32_t cnt = (lane < nc) ? A.count_in[c0 + lane] : 0u;
-    const uint32_t k = min(cnt, A.cap);
-    uint32_t incl = (k + 3u) & ~3u;
+// ------------------------------------------------------- the step kernel --
+// Persistent and warp-specialised.  CTA b walks tiles b, b + G, ...  Warp 8
+// (producer) prepares tiles ahead of the others: reads the tile's counts,
+// lays out its records in shared memory (each cell padded to a multiple of 4
+// slots), writes the slot -> cell table, issues one cp.async.bulk (TMA) per
+// cell and record array, zeroes the consumed counts and draws the cells'
+// rotation axes.  Warps 0-7 (consumers) collide the tile from shared memory
+// and write every particle into its next-step cell.  Two tile buffers with
+// full / empty mbarriers; the consumers synchronise among themselves with a
+// named barrier, never with the producer.
+constexpr int kMaxPT = 512;            // padded record slots per tile in shared memory
+constexpr int kNC = 256;               // consumer threads
+constexpr int kNTW = kNC + 32;         // + one producer warp
+constexpr int kPPTT = kMaxPT / kNC;
+
+struct TileBuf {
+  PRec p[kMaxPT];
+  VRec v[kMaxPT];
+  double ax[kTC * 3];
+  uint32_t cnt[kTC];
+  uint32_t off[kTC + 1];
+  uint8_t cell[kMaxPT];
+  int skip;  // past the end, or a dense tile (queued for k_step_dense)
+};
+
+template <bool DRIFT>
+struct StepSmem {
+  TileBuf buf[2];
+  double val[kMaxPT * 4];  // staged rows in (cell, id) order; zero in padding
+  uint32_t id[kMaxPT];     // ids in slot order, sentinel in padding
+  double mom[kTC * 4];
+  double post[DRIFT ? kTC * 4 : 1];
+  double com[kTC * 3];
+  double red[(kNC / 32) * 5];
+  uint64_t full[2], empty[2];
+};
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kNC) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ uint32_t tile_count(const StepArgs& A, int64_t tl, int64_t ntiles) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = tl * kTC + lane;
+  return (tl < ntiles && c < A.C) ? __ldcg(A.count_in + c) : 0u;
+}
+
+// Producer warp: lay out tile `tl` in `B` from its counts (one per lane),
+// start its copies, draw its axes.  Completes two arrivals on `full` (one
+// with the byte count, one once the generic writes are done).
+__device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint64_t* full,
+                                             int64_t tl, int64_t ntiles, uint32_t cnt,
+                                             uint64_t pol) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = tl * kTC;
+  const int nc = tl < ntiles ? (int)min((int64_t)kTC, A.C - c0) : 0;
+  const uint32_t k = min(cnt, A.cap);
+  const uint32_t pad = (k + 3u) & ~3u;
+  uint32_t incl = pad;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    s_cnt[lane] = cnt;
-    s_off[lane + 1] = incl;
-    if (lane == 0) s_off[0] = 0;
-    const bool over = __any_sync(0xffffffffu, cnt > A.cap);
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 0) s_dense = (over || total > (uint32_t)kMaxP) ? 1 : 0;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  __syncthreads();
-  if (s_dense) {  // rare: the dense kernel handles this tile
-    if (t == 0) A.dense[atomicAdd(&A.flags[0], 1u)] = (uint32_t)tile;
+  const uint32_t excl = incl - pad;
+  const bool over = __any_sync(0xffffffffu, cnt > A.cap);
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const bool skip = tl >= ntiles || over || total > (uint32_t)kMaxPT;
+  B.cnt[lane] = cnt;
+  B.off[lane + 1] = incl;
+  if (lane == 0) {
+    B.off[0] = 0;
+    B.skip = skip ? 1 : 0;
+    if (skip && tl < ntiles) A.dense[atomicAdd(&A.flags[0], 1u)] = (uint32_t)tl;
+  }
+  if (skip) {
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive_expect(full, 0u);
+      mbar_arrive(full);
+    }
     return;
   }
-  const int npad = (int)s_off[nc];
-  if (t < nc) {
-    // slot -> cell table; sentinel ids in the padding (they never rank below)
-    const uint32_t lo = s_off[t], k = s_cnt[t], hi = s_off[t + 1];
-    for (uint32_t j = lo; j < hi; ++j) s_cell[j] = (uint8_t)t;
-    for (uint32_t j = lo + k; j < hi; ++j) s_id[j] = kSentinel;
-    A.count_in[c0 + t] = 0u;  // consumed: this array is the count_out of step k+1
+  const uint32_t bytes = k * (uint32_t)sizeof(PRec);
+  uint32_t sum = 2u * bytes;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) {
+    fence_proxy_async();  // the consumers' generic reads of B precede the async writes
+    mbar_arrive_expect(full, sum);
+  }
+  __syncwarp();
+  if (k) {
+    const uint64_t src = (uint64_t)(c0 + lane) * A.cap;
+    bulk_load(B.p + excl, A.in.p + src, bytes, full, pol);
+    bulk_load(B.v + excl, A.in.v + src, bytes, full, pol);
+  }
+  if (lane < nc) A.count_in[c0 + lane] = 0u;  // consumed: the count_out of step k+1
+  for (uint32_t j = excl; j < incl; ++j) B.cell[j] = (uint8_t)lane;
+  // rotation axes (collision.py:217-250), keyed by the global cell id
+  double* ax = B.ax + lane * 3;
+  ax[0] = ax[1] = ax[2] = 0.0;
+  if (cnt > 0u && !rotation_axis(A.prng, A.seed, A.step, (uint64_t)(c0 + lane), ax))
+    atomicOr(&A.flags[1], 1u);
+  __syncwarp();
+  if (lane == 0) mbar_arrive(full);  // release: layout, table and axes written
+}
+
+template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
+__global__ void __launch_bounds__(kNTW, 2) k_step(const StepArgs A, int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t G = gridDim.x;
+  if (t == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.full[b], 2);
+      mbar_init(&S.empty[b], kNC / 32);
+    }
+    fence_mbar_init();
   }
   __syncthreads();
 
-  // phase 1: issue the loads of (z, id) and the velocity record of every
-  // particle; warp 0 draws the cells' rotation axes while they are in flight
-  double vx[kPPT], vy[kPPT], vz[kPPT], pz[kPPT], mm[kPPT];
-  uint32_t pid[kPPT];
-  int lcell[kPPT];
-  uint64_t src[kPPT];
+  if (warp == kNC / 32) {  // ------------------------------------ producer
+    const uint64_t pol = policy_evict_first();
+    int64_t tile = blockIdx.x;
+    uint32_t cnt = tile_count(A, tile, ntiles);
+    for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
+      const int b = (int)(i & 1);
+      const uint32_t cnt_next = tile_count(A, tile + G, ntiles);  // in flight meanwhile
+      if (i >= 2) mbar_wait(&S.empty[b], (uint32_t)((i >> 1) - 1) & 1u);
+      prepare_tile(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
+      cnt = cnt_next;
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------- consumers
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // px py pz sum(m v^2) mass
+  int64_t tile = blockIdx.x;
+  for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
+    const int b = (int)(i & 1);
+    TileBuf& T = S.buf[b];
+    mbar_wait(&S.full[b], (uint32_t)(i >> 1) & 1u);
+    if (T.skip) {
+      consumer_sync();
+      if (lane == 0) mbar_arrive(&S.empty[b]);
+      continue;
+    }
+    const int64_t c0 = tile * kTC;
+    const int nc = (int)min((int64_t)kTC, A.C - c0);
+    const int npad = (int)T.off[nc];
+
+    // phase 1: ids in slot order (sentinel in the padding); zero padding rows
+    int lcell[kPPTT];
+    bool real[kPPTT];
 #pragma unroll
-  for (int r = 0; r < kPPT; ++r) {
-    const int j = r * kNT + t;
-    pid[r] = kSentinel;
-    lcell[r] = 0;
-    if (j < npad) {
-      const int lc = s_cell[j];
-      const uint32_t s = (uint32_t)j - s_off[lc];
-      lcell[r] = lc;
-      if (s < s_cnt[lc]) {
-        src[r] = (uint64_t)(c0 + lc) * A.cap + s;
-        const double2 zi = ld2cs(&A.in.p[src[r]].z);
-        const double2 v01 = ld2cs(&A.in.v[src[r]].vx);
-        const double2 v2m = ld2cs(&A.in.v[src[r]].vz);
-        pz[r] = zi.x;
-        pid[r] = bits_id(zi.y);
-        vx[r] = v01.x; vy[r] = v01.y; vz[r] = v2m.x;
-        mm[r] = UMASS ? A.m0 : v2m.y;
+    for (int r = 0; r < kPPTT; ++r) {
+      const int j = r * kNC + t;
+      real[r] = false;
+      lcell[r] = 0;
+      if (j < npad) {
+        const int lc = T.cell[j];
+        lcell[r] = lc;
+        real[r] = (uint32_t)j - T.off[lc] < T.cnt[lc];
+        S.id[j] = real[r] ? T.p[j].id : kSentinel;
+        if (!real[r]) {
+          double2* sv = reinterpret_cast<double2*>(S.val + j * 4);
+          sv[0] = make_double2(0.0, 0.0);
+          sv[1] = make_double2(0.0, 0.0);
+        }
       }
     }
-  }
-  if (t < nc) {  // collision.py:217-250, keyed by the global cell id
-    double* ax = s_cx + t * 6 + 3;
-    ax[0] = ax[1] = ax[2] = 0.0;
-    if (s_cnt[t] > 0u && !rotation_axis(A.prng, A.seed, A.step, (uint64_t)(c0 + t), ax))
-      atomicOr(&A.flags[1], 1u);
-  }
-#pragma unroll
-  for (int r = 0; r < kPPT; ++r)
-    if (pid[r] != kSentinel) s_id[r * kNT + t] = pid[r];
-  __syncthreads();
+    consumer_sync();
 
-  // phase 2: rank by id inside the cell (4-wide over the padded segment);
-  // stage (m v, m) in rank order -- the reference permutation is the stable
-  // argsort over id order (collision.py:98)
-  int slot[kPPT];
+    // phase 2: rank by id inside the cell, 4-wide over the padded segment;
+    // stage (m v, m) in rank order -- the reference permutation is the stable
+    // argsort over id order (collision.py:98)
+    int slot[kPPTT];
 #pragma unroll
-  for (int r = 0; r < kPPT; ++r) {
-    slot[r] = 0;
-    if (pid[r] != kSentinel) {
-      const int lc = lcell[r];
-      const int lo = (int)s_off[lc], hi = (int)s_off[lc + 1];
-      const uint32_t me = pid[r];
-      int rank = 0;
-      for (int q = lo; q < hi; q += 4) {
-        const uint4 w = *reinterpret_cast<const uint4*>(s_id + q);
-        rank += (int)(w.x < me) + (int)(w.y < me) + (int)(w.z < me) + (int)(w.w < me);
+    for (int r = 0; r < kPPTT; ++r) {
+      slot[r] = 0;
+      if (real[r]) {
+        const int j = r * kNC + t;
+        const int lc = lcell[r];
+        const int lo = (int)T.off[lc], hi = (int)T.off[lc + 1];
+        const uint32_t me = S.id[j];
+        uint32_t rank = 0;
+        for (int q = lo; q < hi; q += 4) {
+          const uint4 w = *reinterpret_cast<const uint4*>(S.id + q);
+          rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
+        }
+        slot[r] = lo + (int)rank;
+        const VRec v = T.v[j];
+        const double m = UMASS ? A.m0 : v.m;
+        double2* sv = reinterpret_cast<double2*>(S.val + slot[r] * 4);
+        sv[0] = make_double2(m * v.vx, m * v.vy);
+        sv[1] = make_double2(m * v.vz, m);
       }
-      slot[r] = lo + rank;
-      double2* sv = reinterpret_cast<double2*>(s_val + slot[r] * 4);
-      sv[0] = make_double2(mm[r] * vx[r], mm[r] * vy[r]);
-      sv[1] = make_double2(mm[r] * vz[r], mm[r]);
     }
-  }
-  __syncthreads();
+    consumer_sync();
 
-  // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206)
-  for (int task = t; task < nc * 4; task += kNT) {
-    const int lc = task >> 2, comp = task & 3;
-    s_mom[task] = reduceat_col<4>(s_val + s_off[lc] * 4 + comp, (int)min(s_cnt[lc], A.cap));
-  }
-  __syncthreads();
-
-  // phase 4: com = p / m (collision.py:209-214)
-  if (t < nc) {
-    const double mass = s_mom[t * 4 + 3];
-    double* cx = s_cx + t * 6;
-    for (int d = 0; d < 3; ++d) cx[d] = (mass > 0.0) ? s_mom[t * 4 + d] / mass : 0.0;
-    if (COM) {
-      double* g = A.com_cap + (c0 + t) * 4;
-      g[0] = cx[0]; g[1] = cx[1]; g[2] = cx[2]; g[3] = (double)s_cnt[t];
-    }
-  }
-  __syncthreads();
-
-  // phase 5: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
-  // next-step cell; claim every slot, then store; stage post-collision rows
-  double o[kPPT][6];
-  uint32_t key[kPPT];
-#pragma unroll
-  for (int r = 0; r < kPPT; ++r) {
-    key[r] = 0u;
-    if (pid[r] != kSentinel) {
-      const double* cx = s_cx + lcell[r] * 6;
-      double v[3] = {vx[r], vy[r], vz[r]}, w[3];
-      rotate(v, cx, cx + 3, A.cs, A.sn, w);
-      const double2 xy = ld2cs(&A.in.p[src[r]].x);  // same sector as (z, id): L2 hit
-      o[r][0] = wrap_fast(xy.x + w[0] * A.dt, A.box0);
-      o[r][1] = wrap_fast(xy.y + w[1] * A.dt, A.box1);
-      o[r][2] = wrap_fast(pz[r] + w[2] * A.dt, A.box2);
-      o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
-      key[r] = BYID ? pid[r] : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
-      const double m = mm[r];
-      double2* sv = reinterpret_cast<double2*>(s_val + slot[r] * 4);
-      sv[0] = make_double2(m * w[0], m * w[1]);
-      sv[1] = make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]));
-    }
-  }
-  if (BYID) {
-#pragma unroll
-    for (int r = 0; r < kPPT; ++r)
-      if (pid[r] != kSentinel)
-        store_rec(A.out, pid[r], o[r][0], o[r][1], o[r][2], pid[r], o[r][3], o[r][4], o[r][5],
-                  UMASS ? A.m0 : mm[r]);
-  } else {
-    unsigned grp[kPPT];
-    uint32_t base[kPPT];
-#pragma unroll
-    for (int r = 0; r < kPPT; ++r) {
-      grp[r] = 0u;
-      base[r] = 0u;
-      if (r * kNT < npad)  // warp-uniform: every lane takes part in the ballot
-        claim_slot(A, pid[r] != kSentinel, key[r], grp[r], base[r]);
-    }
-#pragma unroll
-    for (int r = 0; r < kPPT; ++r)
-      if (pid[r] != kSentinel)
-        finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], UMASS ? A.m0 : mm[r]);
-  }
-  __syncthreads();
-
-  // phase 6: tile partials (fixed order: deterministic) and drift
-  if (DRIFT) {
-    for (int task = t; task < nc * 4; task += kNT) {
+    // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206)
+    for (int task = t; task < nc * 4; task += kNC) {
       const int lc = task >> 2, comp = task & 3;
-      s_post[task] = reduceat_col<4>(s_val + s_off[lc] * 4 + comp, (int)min(s_cnt[lc], A.cap));
+      S.mom[task] = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
     }
-    __syncthreads();
-    if (t < 5) {
-      double s = 0.0;
-      for (int lc = 0; lc < nc; ++lc) s += (t < 4) ? s_post[lc * 4 + t] : s_mom[lc * 4 + 3];
-      A.partials[tile * 8 + t] = s;
+    consumer_sync();
+
+    // phase 4: com = p / m (collision.py:209-214); cell masses into the sums
+    if (t < nc) {
+      const double mass = S.mom[t * 4 + 3];
+      acc[4] += mass;
+      double* cx = S.com + t * 3;
+      for (int d = 0; d < 3; ++d) cx[d] = (mass > 0.0) ? S.mom[t * 4 + d] / mass : 0.0;
+      if (COM) {
+        double* g = A.com_cap + (c0 + t) * 4;
+        g[0] = cx[0]; g[1] = cx[1]; g[2] = cx[2]; g[3] = (double)T.cnt[t];
+      }
     }
-    if (t >= 32 && t < 64) {
-      double worst = 0.0;
-      for (int lc = t - 32; lc < nc; lc += 32)
-        if (s_mom[lc * 4 + 3] > 0.0) worst = fmax(worst, cell_drift(s_mom + lc * 4, s_post + lc * 4));
-      for (int off = 16; off > 0; off >>= 1)
-        worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
-      if (t == 32 && worst > 0.0) atomic_max_pos_double(A.drift_bits, worst);
-    }
-  } else {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int lc = t >> 5; lc < nc; lc += kNT / 32) {  // warp w: cells w, w + 8, ...
-      const int lo = (int)s_off[lc], k = (int)min(s_cnt[lc], A.cap);
-      for (int j = lo + lane; j < lo + k; j += 32)
+    consumer_sync();
+
+    // phase 5: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
+    // next-step cell; claim every slot, then store; stage post-collision rows
+    double o[kPPTT][6];
+    uint32_t key[kPPTT];
+    double mm[kPPTT];
+    uint32_t pid[kPPTT];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] += s_val[j * 4 + q];
+    for (int r = 0; r < kPPTT; ++r) {
+      key[r] = 0u;
+      if (real[r]) {
+        const int j = r * kNC + t;
+        const PRec p = T.p[j];
+        const VRec vr = T.v[j];
+        const double* cx = S.com + lcell[r] * 3;
+        const double* ax = T.ax + lcell[r] * 3;
+        double v[3] = {vr.vx, vr.vy, vr.vz}, w[3];
+        rotate(v, cx, ax, A.cs, A.sn, w);
+        o[r][0] = wrap_fast(p.x + w[0] * A.dt, A.box0);
+        o[r][1] = wrap_fast(p.y + w[1] * A.dt, A.box1);
+        o[r][2] = wrap_fast(p.z + w[2] * A.dt, A.box2);
+        o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
+        pid[r] = p.id;
+        mm[r] = UMASS ? A.m0 : vr.m;
+        key[r] = BYID ? p.id : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
+        const double m = mm[r];
+        double2* sv = reinterpret_cast<double2*>(S.val + slot[r] * 4);
+        sv[0] = make_double2(m * w[0], m * w[1]);
+        sv[1] = make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]));
+      }
     }
+    if (BYID) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
-    if (lane == 0)
+      for (int r = 0; r < kPPTT; ++r)
+        if (real[r])
+          store_rec(A.out, pid[r], o[r][0], o[r][1], o[r][2], pid[r], o[r][3], o[r][4], o[r][5],
+                    mm[r]);
+    } else {
+      unsigned grp[kPPTT];
+      uint32_t base[kPPTT];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) s_red[(t >> 5) * 4 + q] = acc[q];
-    __syncthreads();
-    if (t < 4) {
-      double s = 0.0;
-      for (int w = 0; w < kNT / 32; ++w) s += s_red[w * 4 + t];
-      A.partials[tile * 8 + t] = s;
-    } else if (t == 4) {
-      double s = 0.0;
-      for (int lc = 0; lc < nc; ++lc) s += s_mom[lc * 4 + 3];
-      A.partials[tile * 8 + 4] = s;
+      for (int r = 0; r < kPPTT; ++r) {
+        grp[r] = 0u;
+        base[r] = 0u;
+        if (r * kNC < npad)  // warp-uniform: every lane takes part in the ballot
+          claim_slot(A, real[r], key[r], grp[r], base[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < kPPTT; ++r)
+        if (real[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
     }
+    consumer_sync();
+    if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
+
+    // phase 6: conservation sums over this thread's staged rows, in slot
+    // order (fixed: deterministic); drift per cell when captured
+#pragma unroll
+    for (int r = 0; r < kPPTT; ++r) {
+      const int j = r * kNC + t;
+      if (j < npad) {  // padding rows are zero
+        const double2* sv = reinterpret_cast<const double2*>(S.val + j * 4);
+        const double2 a = sv[0], c = sv[1];
+        acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
+      }
+    }
+    if (DRIFT) {
+      for (int task = t; task < nc * 4; task += kNC) {
+        const int lc = task >> 2, comp = task & 3;
+        S.post[task] = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
+      }
+      consumer_sync();
+      if (warp == 1) {
+        double worst = 0.0;
+        for (int lc = lane; lc < nc; lc += 32)
+          if (S.mom[lc * 4 + 3] > 0.0)
+            worst = fmax(worst, cell_drift(S.mom + lc * 4, S.post + lc * 4));
+        for (int off = 16; off > 0; off >>= 1)
+          worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+        if (lane == 0 && worst > 0.0) atomic_max_pos_double(A.drift_bits, worst);
+      }
+    }
+    consumer_sync();  // S.val / S.id are rewritten by the next tile
+  }
+  // CTA partials: fixed-order block reduction of the per-thread sums
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+    for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) S.red[warp * 5 + q] = acc[q];
+  consumer_sync();
+  if (t < 5) {
+    double s = 0.0;
+    for (int w = 0; w < kNC / 32; ++w) s += S.red[w * 5 + t];
+    A.partials[(int64_t)blockIdx.x * 8 + t] = s;
   }
 }
 
@@ -466,8 +608,9 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
   const int t = threadIdx.x;
   const uint32_t n_dense = *(volatile uint32_t*)&A.flags[0];
   const uint32_t n_ovf = min(*(volatile uint32_t*)A.ovf_n_in, A.ovf_cap);
+  double dacc = 0.0;  // thread t < 5: this CTA's partial sum of column t
   for (uint32_t e = blockIdx.x; e < n_dense; e += gridDim.x) {
-    const int64_t tile = A.dense[e];
+    const int64_t tile = A.dense[e];  // sorted by k_sort_dense: deterministic sums
     const int64_t c0 = tile * kTC;
     const int nc = (int)min((int64_t)kTC, A.C - c0);
     __syncthreads();
@@ -585,11 +728,8 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       s_post[task] = s_cnt[lc] ? reduceat(g_val + 4 * (uint64_t)s_off[lc] + comp, (int64_t)s_cnt[lc], 4) : 0.0;
     }
     __syncthreads();
-    if (t < 5) {
-      double s = 0.0;
-      for (int lc = 0; lc < nc; ++lc) s += (t < 4) ? s_post[lc * 4 + t] : s_mom[lc * 4 + 3];
-      A.partials[tile * 8 + t] = s;
-    }
+    if (t < 5)
+      for (int lc = 0; lc < nc; ++lc) dacc += (t < 4) ? s_post[lc * 4 + t] : s_mom[lc * 4 + 3];
     if (DRIFT && t >= 32 && t < 64) {
       double worst = 0.0;
       for (int lc = t - 32; lc < nc; lc += 32)
@@ -598,6 +738,20 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       if (t == 32 && worst > 0.0) atomic_max_pos_double(A.drift_bits, worst);
     }
     if (t < nc) A.count_in[c0 + t] = 0u;
+  }
+  if (t < 5) A.partials[(A.part_base + blockIdx.x) * 8 + t] = dacc;
+}
+
+// The dense-tile list is appended in arbitrary order; sort it (ascending) so
+// that each dense CTA's partial sums run over the same tiles every run.
+__global__ void k_sort_dense(uint32_t* list, const uint32_t* flags) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const uint32_t n = flags[0];
+  for (uint32_t i = 1; i < n; ++i) {
+    const uint32_t v = list[i];
+    uint32_t j = i;
+    for (; j > 0 && list[j - 1] > v; --j) list[j] = list[j - 1];
+    list[j] = v;
   }
 }
 
