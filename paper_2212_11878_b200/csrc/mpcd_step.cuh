@@ -87,7 +87,7 @@ struct StepArgs {
   int64_t part_base;          // first partials row of the dense kernel's CTAs
 };
 
-constexpr int kTC = 32;         // cells per tile (one warp owns the per-cell work)
+constexpr int kTC = 16;         // cells per tile (one producer lane per cell)
 constexpr int kNT = 256;        // threads of the step CTA
 constexpr int kPPT = 3;         // staged particles per thread
 constexpr int kMaxP = kNT * kPPT;  // padded staging slots per tile
@@ -279,8 +279,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // and write every particle into its next-step cell.  Two tile buffers with
 // full / empty mbarriers; the consumers synchronise among themselves with a
 // named barrier, never with the producer.
-constexpr int kMaxPT = 512;            // padded record slots per tile in shared memory
-constexpr int kNC = 256;               // consumer threads
+constexpr int kMaxPT = 256;            // padded record slots per tile in shared memory
+constexpr int kNC = 128;               // consumer threads
 constexpr int kNTW = kNC + 32;         // + one producer warp
 constexpr int kPPTT = kMaxPT / kNC;
 
@@ -316,7 +316,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ uint32_t tile_count(const StepArgs& A, int64_t tl, int64_t ntiles) {
   const int lane = threadIdx.x & 31;
   const int64_t c = tl * kTC + lane;
-  return (tl < ntiles && c < A.C) ? __ldcg(A.count_in + c) : 0u;
+  return (lane < kTC && tl < ntiles && c < A.C) ? __ldcg(A.count_in + c) : 0u;
 }
 
 // Producer warp: lay out tile `tl` in `B` from its counts (one per lane),
@@ -340,8 +340,10 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   const bool over = __any_sync(0xffffffffu, cnt > A.cap);
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   const bool skip = tl >= ntiles || over || total > (uint32_t)kMaxPT;
-  B.cnt[lane] = cnt;
-  B.off[lane + 1] = incl;
+  if (lane < kTC) {
+    B.cnt[lane] = cnt;
+    B.off[lane + 1] = incl;
+  }
   if (lane == 0) {
     B.off[0] = 0;
     B.skip = skip ? 1 : 0;
@@ -372,16 +374,18 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane < nc) A.count_in[c0 + lane] = 0u;  // consumed: the count_out of step k+1
   for (uint32_t j = excl; j < incl; ++j) B.cell[j] = (uint8_t)lane;
   // rotation axes (collision.py:217-250), keyed by the global cell id
-  double* ax = B.ax + lane * 3;
-  ax[0] = ax[1] = ax[2] = 0.0;
-  if (cnt > 0u && !rotation_axis(A.prng, A.seed, A.step, (uint64_t)(c0 + lane), ax))
-    atomicOr(&A.flags[1], 1u);
+  if (lane < kTC) {
+    double* ax = B.ax + lane * 3;
+    ax[0] = ax[1] = ax[2] = 0.0;
+    if (cnt > 0u && !rotation_axis(A.prng, A.seed, A.step, (uint64_t)(c0 + lane), ax))
+      atomicOr(&A.flags[1], 1u);
+  }
   __syncwarp();
   if (lane == 0) mbar_arrive(full);  // release: layout, table and axes written
 }
 
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
-__global__ void __launch_bounds__(kNTW, 2) k_step(const StepArgs A, int64_t ntiles) {
+__global__ void __launch_bounds__(kNTW, 4) k_step(const StepArgs A, int64_t ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -460,6 +464,7 @@ __global__ void __launch_bounds__(kNTW, 2) k_step(const StepArgs A, int64_t ntil
         const int lo = (int)T.off[lc], hi = (int)T.off[lc + 1];
         const uint32_t me = S.id[j];
         uint32_t rank = 0;
+#pragma unroll 1
         for (int q = lo; q < hi; q += 4) {
           const uint4 w = *reinterpret_cast<const uint4*>(S.id + q);
           rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
