@@ -46,10 +46,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=None, out: str | None = None) -> str:
+    """Compile libmpcd.so (or a tuning variant with -D`defines` into `out`)."""
+    target = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", LIB + ".tmp", *sources()]
+    flags = [f"-D{d}" for d in (defines or [])]
+    cmd = [nvcc(), *NVCC_FLAGS, *flags, "-I", INCLUDE, "-I", CSRC, "-o", target + ".tmp", *sources()]
     env = dict(os.environ)
     # the distro g++ is the host compiler nvcc 12.9 supports here
     if os.path.exists("/usr/bin/g++"):
@@ -57,8 +60,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, env=env)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

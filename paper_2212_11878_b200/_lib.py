@@ -102,11 +102,12 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("MPCD_LIB", LIB_PATH)  # tuning variants (tools/tune.py)
+    if not os.path.exists(path):
         raise MpcdError(
-            f"CUDA extension not built: {LIB_PATH} is missing. Run "
+            f"CUDA extension not built: {path} is missing. Run "
             "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a).")
-    lib = C.CDLL(LIB_PATH)
+    lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

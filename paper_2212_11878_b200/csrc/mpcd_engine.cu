@@ -432,6 +432,7 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.seed = g.seed;
   A.step = (uint64_t)step;
   A.prng = g.prng;
+  A.axis_prefix = key_prefix(g.seed, (uint64_t)step, kAxis);
   A.m0 = g.mass_value;
   A.part_base = 0;
   (void)by_id;

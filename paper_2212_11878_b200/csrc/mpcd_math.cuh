@@ -49,24 +49,37 @@ MPCD_HD double uniform_at(uint64_t state, uint64_t index) {
   return (double)(mix64(state ^ ((index + 1ULL) * kSeq)) >> 11) * kInv53;
 }
 
-// A keyed stream of doubles in [0,1).  kind == kSplitmix is the reference's
-// counter generator (draw j == uniform_at(key, j)); the sequential
-// generators (not in the reference) are seeded from the
-// same key and consumed in draw order, so draw j plays the role of counter j.
-struct Stream {
-  int kind;
+// Key state after absorbing (seed, step, purpose): the last absorb
+// (rng.py:76) is the only per-cell part, so kernels receive this prefix.
+MPCD_HD uint64_t key_prefix(uint64_t seed, uint64_t step, uint64_t purpose) {
+  uint64_t s = mix64(seed * kSeq + kGolden);
+  s = mix64(s ^ (step * kSeq + kGolden));
+  return mix64(s ^ (purpose * kSeq + kGolden));
+}
+MPCD_HD uint64_t key_from_prefix(uint64_t prefix, uint64_t cell) {
+  return mix64(prefix ^ (cell * kSeq + kGolden));
+}
+
+// A keyed stream of doubles in [0,1), one type per generator (compile-time,
+// so no other generator's code is ever predicated in).  KIND == kSplitmix is
+// the reference's counter generator (draw j == uniform_at(key, j)); the
+// sequential generators (not in the reference) are
+// seeded from the same key and consumed in draw order, so draw j plays the
+// role of counter j.
+template <int KIND>
+struct KStream {
   uint64_t s0, s1, s2, s3;
 
-  MPCD_HD Stream(int k, uint64_t key) : kind(k), s0(key), s1(0), s2(0), s3(0) {
-    if (kind == kMinstd) {
+  MPCD_HD explicit KStream(uint64_t key) : s0(key), s1(0), s2(0), s3(0) {
+    if (KIND == kMinstd) {
       s0 = 1ULL + key % 2147483646ULL;  // x0 in [1, m-1]
-    } else if (kind == kPcg32) {        // pcg32_srandom_r(key, 54)
+    } else if (KIND == kPcg32) {        // pcg32_srandom_r(key, 54)
       s0 = 0;
       s1 = (54ULL << 1) | 1ULL;
       pcg_next();
       s0 += key;
       pcg_next();
-    } else if (kind == kSfc64) {  // a = b = c = key, counter = 1, 12 discards
+    } else if (KIND == kSfc64) {  // a = b = c = key, counter = 1, 12 discards
       s1 = key;
       s2 = key;
       s3 = 1;
@@ -97,21 +110,41 @@ struct Stream {
     return t;
   }
   MPCD_HD double next() {
+    if (KIND == kMinstd) {
+      uint64_t hi = (uint64_t)(minstd_next() - 1u) >> 4;  // 27 bits
+      uint64_t lo = (uint64_t)(minstd_next() - 1u) >> 5;  // 26 bits
+      return (double)((hi << 26) | lo) * kInv53;
+    } else if (KIND == kPcg32) {
+      uint64_t hi = pcg_next() >> 5;
+      uint64_t lo = pcg_next() >> 6;
+      return (double)((hi << 26) | lo) * kInv53;
+    } else if (KIND == kSfc64) {
+      return (double)(sfc_next() >> 11) * kInv53;
+    } else {
+      return uniform_at(s0, s1++);
+    }
+  }
+};
+
+// Runtime-kind stream for host helpers and the stage API (not hot).
+struct Stream {
+  int kind;
+  KStream<kSplitmix> a;
+  KStream<kMinstd> b;
+  KStream<kPcg32> c;
+  KStream<kSfc64> d;
+  MPCD_HD Stream(int k, uint64_t key)
+      : kind(k),
+        a(key),
+        b(k == kMinstd ? key : 1ULL),
+        c(k == kPcg32 ? key : 0ULL),
+        d(k == kSfc64 ? key : 0ULL) {}
+  MPCD_HD double next() {
     switch (kind) {
-      case kMinstd: {
-        uint64_t hi = (uint64_t)(minstd_next() - 1u) >> 4;  // 27 bits
-        uint64_t lo = (uint64_t)(minstd_next() - 1u) >> 5;  // 26 bits
-        return (double)((hi << 26) | lo) * kInv53;
-      }
-      case kPcg32: {
-        uint64_t hi = pcg_next() >> 5;
-        uint64_t lo = pcg_next() >> 6;
-        return (double)((hi << 26) | lo) * kInv53;
-      }
-      case kSfc64:
-        return (double)(sfc_next() >> 11) * kInv53;
-      default:
-        return uniform_at(s0, s1++);
+      case kMinstd: return b.next();
+      case kPcg32: return c.next();
+      case kSfc64: return d.next();
+      default: return a.next();
     }
   }
 };
@@ -124,8 +157,9 @@ MPCD_HD void grid_shift(int kind, uint64_t seed, uint64_t step, double a, double
 
 // collision.py:217-250 for one cell: Marsaglia rejection, first accepted
 // trial wins.  Returns false if 128 trials all failed (reference raises).
-MPCD_HD bool rotation_axis(int kind, uint64_t seed, uint64_t step, uint64_t cell, double ax[3]) {
-  Stream g(kind, key_state(seed, step, kAxis, cell));
+template <int KIND>
+MPCD_HD bool rotation_axis_k(uint64_t key, double ax[3]) {
+  KStream<KIND> g(key);
   for (int t = 0; t < kMaxAxisTrials; ++t) {
     double x = 2.0 * g.next() - 1.0;
     double y = 2.0 * g.next() - 1.0;
@@ -140,6 +174,22 @@ MPCD_HD bool rotation_axis(int kind, uint64_t seed, uint64_t step, uint64_t cell
   }
   ax[0] = ax[1] = ax[2] = 0.0;
   return false;
+}
+
+// The axis of `cell` from the per-step prefix (key_prefix(seed, step, kAxis));
+// the generator branch is uniform across a launch.
+MPCD_HD bool rotation_axis_pre(int kind, uint64_t prefix, uint64_t cell, double ax[3]) {
+  const uint64_t key = key_from_prefix(prefix, cell);
+  switch (kind) {
+    case kMinstd: return rotation_axis_k<kMinstd>(key, ax);
+    case kPcg32: return rotation_axis_k<kPcg32>(key, ax);
+    case kSfc64: return rotation_axis_k<kSfc64>(key, ax);
+    default: return rotation_axis_k<kSplitmix>(key, ax);
+  }
+}
+
+MPCD_HD bool rotation_axis(int kind, uint64_t seed, uint64_t step, uint64_t cell, double ax[3]) {
+  return rotation_axis_pre(kind, key_prefix(seed, step, kAxis), cell, ax);
 }
 
 // collision.py:289-306 (Rodrigues), numpy order:

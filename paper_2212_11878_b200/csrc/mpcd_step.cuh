@@ -82,12 +82,25 @@ struct StepArgs {
   double a, dt, cs, sn, box0, box1, box2;
   double off_next0, off_next1, off_next2;
   uint64_t seed, step;
+  uint64_t axis_prefix;       // key_prefix(seed, step, AXIS)
   int prng;
   double m0;
   int64_t part_base;          // first partials row of the dense kernel's CTAs
 };
 
-constexpr int kTC = 16;         // cells per tile (one producer lane per cell)
+#ifndef MPCD_TC
+#define MPCD_TC 16
+#endif
+#ifndef MPCD_NC
+#define MPCD_NC 128
+#endif
+#ifndef MPCD_MAXPT
+#define MPCD_MAXPT 256
+#endif
+#ifndef MPCD_MINB
+#define MPCD_MINB 4
+#endif
+constexpr int kTC = MPCD_TC;    // cells per tile (one producer lane per cell, <= 32)
 constexpr int kNT = 256;        // threads of the step CTA
 constexpr int kPPT = 3;         // staged particles per thread
 constexpr int kMaxP = kNT * kPPT;  // padded staging slots per tile
@@ -279,8 +292,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // and write every particle into its next-step cell.  Two tile buffers with
 // full / empty mbarriers; the consumers synchronise among themselves with a
 // named barrier, never with the producer.
-constexpr int kMaxPT = 256;            // padded record slots per tile in shared memory
-constexpr int kNC = 128;               // consumer threads
+constexpr int kMaxPT = MPCD_MAXPT;     // padded record slots per tile in shared memory
+constexpr int kNC = MPCD_NC;           // consumer threads
 constexpr int kNTW = kNC + 32;         // + one producer warp
 constexpr int kPPTT = kMaxPT / kNC;
 
@@ -377,7 +390,7 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane < kTC) {
     double* ax = B.ax + lane * 3;
     ax[0] = ax[1] = ax[2] = 0.0;
-    if (cnt > 0u && !rotation_axis(A.prng, A.seed, A.step, (uint64_t)(c0 + lane), ax))
+    if (cnt > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, (uint64_t)(c0 + lane), ax))
       atomicOr(&A.flags[1], 1u);
   }
   __syncwarp();
@@ -385,7 +398,7 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
 }
 
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
-__global__ void __launch_bounds__(kNTW, 4) k_step(const StepArgs A, int64_t ntiles) {
+__global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int64_t ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -529,6 +542,8 @@ __global__ void __launch_bounds__(kNTW, 4) k_step(const StepArgs A, int64_t ntil
         sv[1] = make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]));
       }
     }
+    unsigned grp[kPPTT];
+    uint32_t base[kPPTT];
     if (BYID) {
 #pragma unroll
       for (int r = 0; r < kPPTT; ++r)
@@ -536,8 +551,6 @@ __global__ void __launch_bounds__(kNTW, 4) k_step(const StepArgs A, int64_t ntil
           store_rec(A.out, pid[r], o[r][0], o[r][1], o[r][2], pid[r], o[r][3], o[r][4], o[r][5],
                     mm[r]);
     } else {
-      unsigned grp[kPPTT];
-      uint32_t base[kPPTT];
 #pragma unroll
       for (int r = 0; r < kPPTT; ++r) {
         grp[r] = 0u;
@@ -545,15 +558,12 @@ __global__ void __launch_bounds__(kNTW, 4) k_step(const StepArgs A, int64_t ntil
         if (r * kNC < npad)  // warp-uniform: every lane takes part in the ballot
           claim_slot(A, real[r], key[r], grp[r], base[r]);
       }
-#pragma unroll
-      for (int r = 0; r < kPPTT; ++r)
-        if (real[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
     }
     consumer_sync();
     if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
 
     // phase 6: conservation sums over this thread's staged rows, in slot
-    // order (fixed: deterministic); drift per cell when captured
+    // order (fixed: deterministic) -- while the slot claims are in flight
 #pragma unroll
     for (int r = 0; r < kPPTT; ++r) {
       const int j = r * kNC + t;
@@ -562,6 +572,11 @@ __global__ void __launch_bounds__(kNTW, 4) k_step(const StepArgs A, int64_t ntil
         const double2 a = sv[0], c = sv[1];
         acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
       }
+    }
+    if (!BYID) {
+#pragma unroll
+      for (int r = 0; r < kPPTT; ++r)
+        if (real[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
     }
     if (DRIFT) {
       for (int task = t; task < nc * 4; task += kNC) {
@@ -695,7 +710,7 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       double* cx = s_cx + t * 6;
       for (int d = 0; d < 3; ++d) cx[d] = (mass > 0.0) ? s_mom[t * 4 + d] / mass : 0.0;
       cx[3] = cx[4] = cx[5] = 0.0;
-      if (s_cnt[t] > 0u && !rotation_axis(A.prng, A.seed, A.step, (uint64_t)(c0 + t), cx + 3))
+      if (s_cnt[t] > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, (uint64_t)(c0 + t), cx + 3))
         atomicOr(&A.flags[1], 1u);
       if (COM) {
         double* g = A.com_cap + (c0 + t) * 4;
