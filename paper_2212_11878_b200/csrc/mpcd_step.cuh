@@ -493,21 +493,20 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     consumer_sync();
 
     // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206)
-    for (int task = t; task < nc * 4; task += kNC) {
-      const int lc = task >> 2, comp = task & 3;
-      S.mom[task] = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
-    }
-    consumer_sync();
-
-    // phase 4: com = p / m (collision.py:209-214); cell masses into the sums
-    if (t < nc) {
-      const double mass = S.mom[t * 4 + 3];
-      acc[4] += mass;
-      double* cx = S.com + t * 3;
-      for (int d = 0; d < 3; ++d) cx[d] = (mass > 0.0) ? S.mom[t * 4 + d] / mass : 0.0;
-      if (COM) {
-        double* g = A.com_cap + (c0 + t) * 4;
-        g[0] = cx[0]; g[1] = cx[1]; g[2] = cx[2]; g[3] = (double)T.cnt[t];
+    // four lanes per cell; com = p / m (collision.py:209-214) from the
+    // group's mass lane by shuffle, so no barrier separates the two
+    static_assert(kNC >= 4 * kTC, "one moment task per consumer thread");
+    {
+      const int lc = t >> 2, comp = t & 3;
+      double mom = 0.0;
+      if (lc < nc) mom = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
+      const double mass = __shfl_sync(0xffffffffu, mom, lane | 3);
+      if (lc < nc) {
+        S.mom[t] = mom;
+        const double q = (comp < 3) ? ((mass > 0.0) ? mom / mass : 0.0) : (double)T.cnt[lc];
+        if (comp < 3) S.com[lc * 3 + comp] = q;
+        else acc[4] += mass;
+        if (COM) A.com_cap[(c0 + lc) * 4 + comp] = q;
       }
     }
     consumer_sync();
