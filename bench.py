@@ -41,7 +41,9 @@ PPC = 10.0
 # per cell it reads + zeroes this step's count, updates the next count
 # (atomic, 8) and writes 64 B of partials per 32-cell tile.
 KERNELS = ("k_step", "k_step_dense", "k_diag")  # mpcd_read_profile slots 0..2
-LAUNCHES_PER_STEP = 4  # k_step, k_step_dense, k_diag_partial, k_diag_finalize
+# k_step, k_sort_dense, k_step_dense, k_diag_partial, k_diag_finalize
+# (+ k_place_xrecs, the absorb of received particles, in a decomposed box)
+LAUNCHES_PER_STEP = 5
 BYTES_PER_N = {"k_step": 128, "k_step_dense": 0, "k_diag": 0}
 BYTES_PER_C = {"k_step": 16 + 64.0 / 32, "k_step_dense": 0, "k_diag": 64.0 / 32}
 SURVEY_B_ALG_N, SURVEY_B_ALG_C = 216, 28  # B_alg = 216 n + 28 C
@@ -196,23 +198,53 @@ def run_ours(args):
     import torch
 
     ws, rank, local = dist_setup(args)
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # MPCD_BENCH_BACKEND=gloo: host-staged exchange, lets several ranks
+        # share one GPU (a functional check of this path, not a bench number)
+        backend = os.environ.get("MPCD_BENCH_BACKEND", "nccl")
+        kw = {"device_id": torch.device("cuda", local)} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
     from paper_2212_11878_b200 import _lib
     from paper_2212_11878_b200.engine import EngineContext
     from paper_2212_11878_b200.params import SimParams
 
     L = args.L
-    params = SimParams(edge_length=L, seed=args.seed + rank)
-    n = params.n_particles
-    C = params.n_cells
-    ctx = EngineContext(params.dims, params.cell_size, params.dt, params.alpha, params.seed,
-                        params.prng, n, mass_value=1.0)
-    ctx.init_device(n, 1.0, 0)
     stream = torch.cuda.current_stream()
-    ctx.run(0, args.warmup)
+    if ws == 1:
+        # BASELINE config 3: one 256^3 periodic box, no collective
+        params = SimParams(edge_length=L, seed=args.seed)
+        n = params.n_particles
+        ctx = EngineContext(params.dims, params.cell_size, params.dt, params.alpha, params.seed,
+                            params.prng, n, mass_value=1.0)
+        ctx.init_device(n, 1.0, 0)
+        n_total = n
+
+        def run_steps(first, count):
+            ctx.run(first, count)  # no host synchronisation between steps
+    else:
+        # BASELINE config 4: (L*ws) x L x L box, slab-decomposed, L^3 cells per
+        # GPU, particle migration over NCCL every step
+        from paper_2212_11878_b200.distributed import CudaDomain, DistExchange, DomainLayout
+        dims = (L * ws, L, L)
+        params = SimParams(edge_length=dims[0], edge_lengths=dims, seed=args.seed,
+                           rank_dims=(ws, 1, 1))
+        layout = DomainLayout.from_params(params)
+        dom = CudaDomain(params, layout, rank)
+        dom.init_device(params.n_particles, 1.0)
+        ctx = dom.ctx
+        exch = DistExchange()
+        n_total = params.n_particles
+        n = n_total // ws
+
+        def run_steps(first, count):
+            for k in range(first, first + count):
+                dom.step(k, 0)
+                exch.exchange([dom])
+    C = L ** 3
+    run_steps(0, args.warmup)
     torch.cuda.synchronize()
 
     def barrier():
@@ -225,7 +257,7 @@ def run_ours(args):
         barrier()
         torch.cuda.synchronize()
         start.record(stream)
-        ctx.run(args.warmup, args.steps)
+        run_steps(args.warmup, args.steps)
         end.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -234,7 +266,7 @@ def run_ours(args):
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = ws * n / (ms * 1e-3)
+    value = n_total / (ms * 1e-3)
     d = ctx.read_diag()
 
     # per-kernel timing (CUDA events on the engine stream), separate pass
@@ -242,7 +274,7 @@ def run_ours(args):
     lib = _lib.load()
     lib.mpcd_profile(ctx.handle, 1)
     prof_steps = max(3, min(args.steps, 10))
-    ctx.run(args.warmup + args.steps, prof_steps)
+    run_steps(args.warmup + args.steps, prof_steps)
     kms = (C_.c_double * 5)()
     nst = C_.c_int64(0)
     _lib.check(lib.mpcd_read_profile(ctx.handle, kms, C_.byref(nst)))
@@ -275,7 +307,8 @@ def run_ours(args):
                                "dt 0.1, splitmix keyed RNG",
                    "cells_per_gpu": C, "particles_per_gpu": n,
                    "parallelism": "single domain" if ws == 1 else
-                   f"replicas x{ws} (independent periodic boxes, seed + rank)",
+                   f"slab decomposition ({ws},1,1) of a {L * ws}x{L}x{L} box (BASELINE "
+                   "config 4), particle migration over NCCL every step",
                    "l2": "state 17 GB >> 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -287,12 +320,14 @@ def run_ours(args):
             "survey_b_alg_frac": survey_bytes / (ms * 1e-3) / 1e9 / peak,
             "b_min_frac": B_MIN_N * n / (ms * 1e-3) / 1e9 / peak,
             "kernel_ms": per_kernel},
-        "gpu_launches": args.steps * LAUNCHES_PER_STEP,
+        "gpu_launches": args.steps * (LAUNCHES_PER_STEP + (1 if ws > 1 else 0)),
         "diag_last": {"momentum": list(d.momentum), "energy": d.energy, "mass": d.mass},
     }
     line["clocks"] = clocks.summary()
-    if rank == 0 and not args.no_e2e:
+    if ws == 1 and not args.no_e2e:
         line["e2e"], line["e2e_stateful"] = e2e(args, params, ctx)
+    elif ws > 1 and not args.no_e2e:
+        line["e2e"] = e2e_decomposed(args, params, dom, exch)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_sample_L, 3, args.seed)
     if rank == 0:
@@ -300,6 +335,33 @@ def run_ours(args):
     ctx.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def e2e_decomposed(args, params, dom, exch):
+    """Simulation.step() of the nccl backend (NcclRunner.run_step): step,
+    migration, per-rank diagnostics read back and merged on every rank."""
+    import torch
+
+    from paper_2212_11878_b200.distributed import _DomainRunner
+
+    runner = _DomainRunner(params, [dom], exch, capture_drift=False, capture_com=False)
+    first = int(dom.ctx._lib.mpcd_current_step(dom.ctx.handle))  # a domain steps consecutively
+    runner.run_step(first)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for k in range(args.steps):
+        runner.run_step(first + 1 + k)
+    e.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([s.elapsed_time(e) * 1e-3], device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return {"value": params.n_particles * args.steps / float(t.item()), "unit": UNIT,
+            "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * 9,
+            "api": "Simulation(backend='nccl').step(): state resident, per-rank diagnostics "
+                   "read back and merged every step (no pure-function form for a decomposed box)"}
 
 
 def e2e(args, params, ctx):

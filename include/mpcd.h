@@ -4,8 +4,10 @@
  * Plain C types only (no torch, no C++).  Two layers:
  *
  *  1. Engine context (mpcd_ctx_*): particle state resident in HBM across
- *     steps, sorted by collision cell.  One step is three kernels (collide +
- *     next-step histogram, exclusive scan, collide + scatter).  Replaces the
+ *     steps in fixed-capacity collision-cell regions.  One step is one
+ *     persistent kernel (collide + stream + write each particle into its
+ *     next-step cell) plus a dense-tile kernel and a diagnostics reduction
+ *     (DESIGN.md section 3).  Replaces the
  *     reference's per-step entry point
  *         Simulation.step()                 engine.py:555-591
  *         serial_collision_step(p, params, step, want_drift, want_com)
@@ -155,6 +157,48 @@ int mpcd_init_device(mpcd_ctx* ctx, int64_t n, double velocity_variance, int64_t
 #define MPCD_PROFILE_SLOTS 5
 int mpcd_profile(mpcd_ctx* ctx, int32_t enable);
 int mpcd_read_profile(mpcd_ctx* ctx, double* ms, int64_t* n_steps);
+
+/* ---------------------------------------------- decomposed box (backend nccl)
+ * The reference's parallel path splits the box over a rank grid
+ * (decomposition.py:20-146, SimParams.rank_dims) and runs per-rank phases
+ * with halo moment exchange and particle migration (engine.py:190-272,
+ * exchange.py:225-506).  Here a rank owns the cells of its block of the
+ * SHIFTED grid of each step and every particle in them, so a cell is never
+ * split between ranks: no moment exchange, and the trajectory is
+ * bit-identical to the whole-box step.  After mpcd_step the particles whose
+ * next-step cell belongs to another rank sit in per-destination send
+ * buffers; the caller moves them (NCCL / gloo / device copies) and hands the
+ * received ones to mpcd_absorb before the next step.
+ *
+ * The context's cfg.dims are the domain's cells; global_dims = rank_dims *
+ * dims; rank = (bx * rank_dims[1] + by) * rank_dims[2] + bz owns cells
+ * [b * dims, (b + 1) * dims) per axis.  After set_domain, mpcd_upload and
+ * mpcd_init_device take the WHOLE box's particles and keep this domain's. */
+typedef struct {
+  int64_t global_dims[3];
+  int32_t rank_dims[3];
+  int32_t rank;
+  int64_t send_capacity; /* records per destination rank; 0 = default */
+} mpcd_domain;
+
+/* Send side of the exchange (device pointers owned by the context).
+ * send + (d * send_capacity + i) * record_bytes is the i-th record for rank
+ * d, i < send_n[d] after mpcd_step (send_n[d] > send_capacity means the
+ * buffer overflowed and the step is lost: MPCD_ERR_CAPACITY for the caller).
+ * Record: double x, y, z; uint32 id, pad; double vx, vy, vz, m (64 bytes). */
+typedef struct {
+  void* send;
+  unsigned long long* send_n;
+  int64_t send_capacity;
+  int32_t n_ranks;
+  int32_t record_bytes;
+} mpcd_exchange;
+
+int mpcd_ctx_set_domain(mpcd_ctx* ctx, const mpcd_domain* dom);
+int mpcd_exchange_buffers(mpcd_ctx* ctx, mpcd_exchange* out);
+/* Bin n_recv received DEVICE records for the next step, account for the
+ * n_sent this domain gave away, and clear send_n. */
+int mpcd_absorb(mpcd_ctx* ctx, const void* recs, int64_t n_recv, int64_t n_sent, void* stream);
 
 /* ------------------------------------------------------ host RNG helpers */
 uint64_t mpcd_key_state(uint64_t seed, uint64_t step, uint64_t purpose, uint64_t cell);

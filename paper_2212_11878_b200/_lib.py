@@ -53,6 +53,25 @@ class MpcdDiag(C.Structure):
     ]
 
 
+class MpcdDomain(C.Structure):
+    _fields_ = [
+        ("global_dims", C.c_int64 * 3),
+        ("rank_dims", C.c_int32 * 3),
+        ("rank", C.c_int32),
+        ("send_capacity", C.c_int64),
+    ]
+
+
+class MpcdExchange(C.Structure):
+    _fields_ = [
+        ("send", C.c_void_p),
+        ("send_n", C.c_void_p),
+        ("send_capacity", C.c_int64),
+        ("n_ranks", C.c_int32),
+        ("record_bytes", C.c_int32),
+    ]
+
+
 # name -> (restype, argtypes); mirrors include/mpcd.h one to one
 SIGNATURES = {
     "mpcd_version": (C.c_char_p, []),
@@ -71,6 +90,9 @@ SIGNATURES = {
     "mpcd_read_binning": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _vp]),
     "mpcd_step_host": (C.c_int, [_vp, _d, _d, _d, C.c_int64, C.c_int64, C.c_int32, _d, _vp]),
     "mpcd_init_device": (C.c_int, [_vp, C.c_int64, C.c_double, C.c_int64, _vp]),
+    "mpcd_ctx_set_domain": (C.c_int, [_vp, C.POINTER(MpcdDomain)]),
+    "mpcd_exchange_buffers": (C.c_int, [_vp, C.POINTER(MpcdExchange)]),
+    "mpcd_absorb": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp]),
     "mpcd_profile": (C.c_int, [_vp, C.c_int32]),
     "mpcd_read_profile": (C.c_int, [_vp, _d, _i64]),
     "mpcd_key_state": (C.c_uint64, [C.c_uint64] * 4),

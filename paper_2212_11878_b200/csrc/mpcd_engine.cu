@@ -43,6 +43,10 @@ __device__ __forceinline__ uint32_t flat_cell(double x, double y, double z, doub
 
 struct PlaceArgs {
   Recs reg;
+  // multi-domain: keep only the particles whose cell lies in [org, org + L)
+  // of the global G grid (strict: any other is a routing error, flags[3])
+  int multi, strict;
+  int64_t G0, G1, G2, org0, org1, org2;
   uint32_t* count;
   Recs ovf;
   uint32_t* ovf_cell;
@@ -55,9 +59,23 @@ struct PlaceArgs {
   int64_t L0, L1, L2;
 };
 
-__device__ __forceinline__ void place_one(const PlaceArgs& P, double x, double y, double z,
-                                          uint32_t id, double vx, double vy, double vz, double m) {
-  const uint32_t c = flat_cell(x, y, z, P.o0, P.o1, P.o2, P.a, P.unit, P.L0, P.L1, P.L2);
+// Returns 1 when the particle was placed in this domain.
+__device__ __forceinline__ int place_one(const PlaceArgs& P, double x, double y, double z,
+                                         uint32_t id, double vx, double vy, double vz, double m) {
+  uint32_t c;
+  if (P.multi) {
+    const int64_t lx = pymod(cell_coord(x, P.o0, P.a, P.unit), P.G0) - P.org0;
+    const int64_t ly = pymod(cell_coord(y, P.o1, P.a, P.unit), P.G1) - P.org1;
+    const int64_t lz = pymod(cell_coord(z, P.o2, P.a, P.unit), P.G2) - P.org2;
+    if ((uint64_t)lx >= (uint64_t)P.L0 || (uint64_t)ly >= (uint64_t)P.L1 ||
+        (uint64_t)lz >= (uint64_t)P.L2) {
+      if (P.strict) atomicOr(&P.flags[3], 1u);
+      return 0;
+    }
+    c = (uint32_t)((lx * P.L1 + ly) * P.L2 + lz);
+  } else {
+    c = flat_cell(x, y, z, P.o0, P.o1, P.o2, P.a, P.unit, P.L0, P.L1, P.L2);
+  }
   const uint32_t s = atomicAdd(&P.count[c], 1u);
   if (s < P.cap) {
     store_rec(P.reg, (uint64_t)c * P.cap + s, x, y, z, id, vx, vy, vz, m);
@@ -70,15 +88,56 @@ __device__ __forceinline__ void place_one(const PlaceArgs& P, double x, double y
       atomicOr(&P.flags[2], 1u);
     }
   }
+  return 1;
+}
+
+__device__ __forceinline__ void add_placed(const PlaceArgs& P, uint32_t* placed, uint32_t k) {
+  if (placed && k) atomicAdd(placed, k);
 }
 
 // bin host rows ((n,3) positions/velocities) for step k
-__global__ void k_place_rows(const double* pos, const double* vel, const double* mass,
-                             const int64_t* ids, int64_t n, double m0, PlaceArgs P) {
+// (n,3) rows are read as whole contiguous chunks (kRowBlock rows per block
+// iteration, staged in shared memory), so that the same kernel reads mapped
+// pinned HOST memory over PCIe at full efficiency: the pure-function path
+// bins its input straight from the caller's buffers (no H2D copy pass).
+constexpr int kRowBlock = 256;
+
+__device__ __forceinline__ void load_rows3(double* dst, const double* src, int64_t r0, int rows) {
+  const int64_t base = 3 * r0;
+  const int cnt = 3 * rows;
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) dst[j] = src[base + j];
+}
+
+__global__ void __launch_bounds__(kRowBlock) k_place_rows(const double* pos, const double* vel,
+                                                          const double* mass, const int64_t* ids,
+                                                          int64_t n, double m0, PlaceArgs P,
+                                                          uint32_t* placed) {
+  __shared__ double sp[3 * kRowBlock], sv[3 * kRowBlock];
+  uint32_t k = 0;
+  for (int64_t r0 = (int64_t)blockIdx.x * kRowBlock; r0 < n; r0 += (int64_t)gridDim.x * kRowBlock) {
+    const int rows = (int)min((int64_t)kRowBlock, n - r0);
+    __syncthreads();
+    load_rows3(sp, pos, r0, rows);
+    load_rows3(sv, vel, r0, rows);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < rows) {
+      const int64_t i = r0 + t;
+      k += place_one(P, sp[3 * t], sp[3 * t + 1], sp[3 * t + 2],
+                     ids ? (uint32_t)ids[i] : (uint32_t)i, sv[3 * t], sv[3 * t + 1], sv[3 * t + 2],
+                     mass ? mass[i] : m0);
+    }
+  }
+  add_placed(P, placed, k);
+}
+
+// insert particles received from other domains (64-byte records)
+__global__ void k_place_xrecs(const XRec* r, int64_t n, PlaceArgs P) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    place_one(P, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], ids ? (uint32_t)ids[i] : (uint32_t)i,
-              vel[3 * i], vel[3 * i + 1], vel[3 * i + 2], mass ? mass[i] : m0);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const XRec q = r[i];
+    place_one(P, q.p.x, q.p.y, q.p.z, q.p.id, q.v.vx, q.v.vy, q.v.vz, q.v.m);
+  }
 }
 
 // bin flat records (rows 0..n-1 of a record array) for step k
@@ -128,6 +187,30 @@ __global__ void k_flatten(Recs reg, const uint32_t* count, int64_t C, uint32_t c
 }
 
 // flat records -> host row layout
+// flat records -> (n,3) rows written as contiguous chunks (device or mapped
+// pinned host memory: the pure-function path writes the caller's buffers
+// directly, no D2H copy pass)
+__global__ void __launch_bounds__(kRowBlock) k_flat_to_rows_chunked(Recs flat, int64_t n,
+                                                                    double* pos, double* vel) {
+  __shared__ double sp[3 * kRowBlock], sv[3 * kRowBlock];
+  for (int64_t r0 = (int64_t)blockIdx.x * kRowBlock; r0 < n; r0 += (int64_t)gridDim.x * kRowBlock) {
+    const int rows = (int)min((int64_t)kRowBlock, n - r0);
+    const int t = threadIdx.x;
+    __syncthreads();
+    if (t < rows) {
+      const PRec p = flat.p[r0 + t];
+      const VRec v = flat.v[r0 + t];
+      sp[3 * t] = p.x; sp[3 * t + 1] = p.y; sp[3 * t + 2] = p.z;
+      sv[3 * t] = v.vx; sv[3 * t + 1] = v.vy; sv[3 * t + 2] = v.vz;
+    }
+    __syncthreads();
+    for (int j = t; j < 3 * rows; j += blockDim.x) {
+      pos[3 * r0 + j] = sp[j];
+      vel[3 * r0 + j] = sv[j];
+    }
+  }
+}
+
 __global__ void k_flat_to_rows(Recs flat, int64_t n, double* pos, double* vel, double* mass,
                                int64_t* ids, int uniform_mass, double m0) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -177,24 +260,33 @@ __global__ void k_widen_counts(const uint32_t* count, int64_t C, int64_t* out) {
 }
 
 // particles.py:101-127 on the device: positions exact (integer hash * box),
-// velocities through device log/cos (numpy agrees to ~1 ulp only).
-__global__ void k_init_device(Recs flat, int64_t n, uint64_t state, double b0, double b1,
-                              double b2, double sigma, double m0, double* vsum_partials) {
+// velocities through device log/cos (numpy agrees to ~1 ulp only).  Two
+// passes over the particle ids, so nothing is staged: k_init_sum reduces the
+// velocities (fixed grid and order: every domain of a decomposed box gets the
+// same mean bits), k_init_place regenerates each particle, removes the mean
+// (particles.py mean_init_velocity) and bins it for the first step -- in a
+// decomposed box only the particles of this domain's cells.
+constexpr int kInitBlocks = 148 * 8;
+
+__device__ __forceinline__ void init_velocity(uint64_t state, int64_t n, int64_t i, double sigma,
+                                              double v[3]) {
+  const double two_pi = 2.0 * 3.141592653589793;
+  for (int d = 0; d < 3; ++d) {
+    const uint64_t g = (uint64_t)(3 * n + 3 * i + d);
+    const double u1 = uniform_at(state, 2 * g), u2 = uniform_at(state, 2 * g + 1);
+    v[d] = sqrt(-2.0 * log(1.0 - u1)) * cos(two_pi * u2) * sigma;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_init_sum(int64_t n, uint64_t state, double sigma,
+                                                  double* vsum_partials) {
   __shared__ double s_sum[3][256];
   double acc[3] = {0, 0, 0};
-  const double two_pi = 2.0 * 3.141592653589793;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double v[3];
-    for (int d = 0; d < 3; ++d) {
-      const uint64_t g = (uint64_t)(3 * n + 3 * i + d);
-      const double u1 = uniform_at(state, 2 * g), u2 = uniform_at(state, 2 * g + 1);
-      v[d] = sqrt(-2.0 * log(1.0 - u1)) * cos(two_pi * u2) * sigma;
-      acc[d] += v[d];
-    }
-    store_rec(flat, (uint64_t)i, uniform_at(state, (uint64_t)(3 * i)) * b0,
-              uniform_at(state, (uint64_t)(3 * i + 1)) * b1,
-              uniform_at(state, (uint64_t)(3 * i + 2)) * b2, (uint32_t)i, v[0], v[1], v[2], m0);
+    init_velocity(state, n, i, sigma, v);
+    for (int d = 0; d < 3; ++d) acc[d] += v[d];
   }
   for (int d = 0; d < 3; ++d) s_sum[d][threadIdx.x] = acc[d];
   __syncthreads();
@@ -207,8 +299,11 @@ __global__ void k_init_device(Recs flat, int64_t n, uint64_t state, double b0, d
     for (int d = 0; d < 3; ++d) vsum_partials[blockIdx.x * 3 + d] = s_sum[d][0];
 }
 
-__global__ void k_init_remove_mean(Recs flat, int64_t n, const double* vsum_partials,
-                                   int nblocks) {
+__global__ void __launch_bounds__(256) k_init_place(int64_t n, uint64_t state, double b0,
+                                                    double b1, double b2, double sigma,
+                                                    double m0, const double* vsum_partials,
+                                                    int nblocks, PlaceArgs P,
+                                                    uint32_t* placed) {
   __shared__ double mean[3];
   if (threadIdx.x < 3) {
     double acc = 0.0;
@@ -216,12 +311,17 @@ __global__ void k_init_remove_mean(Recs flat, int64_t n, const double* vsum_part
     mean[threadIdx.x] = n ? acc / (double)n : 0.0;
   }
   __syncthreads();
+  uint32_t k = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    flat.v[i].vx -= mean[0];
-    flat.v[i].vy -= mean[1];
-    flat.v[i].vz -= mean[2];
+    double v[3];
+    init_velocity(state, n, i, sigma, v);
+    k += place_one(P, uniform_at(state, (uint64_t)(3 * i)) * b0,
+                   uniform_at(state, (uint64_t)(3 * i + 1)) * b1,
+                   uniform_at(state, (uint64_t)(3 * i + 2)) * b2, (uint32_t)i, v[0] - mean[0],
+                   v[1] - mean[1], v[2] - mean[2], m0);
   }
+  add_placed(P, placed, k);
 }
 
 }  // namespace mpcd
@@ -261,6 +361,12 @@ struct mpcd_ctx {
   int64_t last_step = -1;
   bool prof = false;
   std::vector<cudaEvent_t> prof_events;
+  // multi-domain (mpcd_ctx_set_domain): cfg.dims are this domain's cells
+  bool multi = false;
+  mpcd_domain dom{};
+  int64_t org[3] = {0, 0, 0};
+  XRec* send = nullptr;
+  unsigned long long* send_n = nullptr;
 };
 
 namespace {
@@ -270,6 +376,7 @@ constexpr int kProfSlots = 3;  // step, step_dense, diagnostics
 uint32_t* flags_of(mpcd_ctx* c) { return c->small; }
 uint32_t* ovf_n_of(mpcd_ctx* c, int b) { return c->small + 4 + b; }
 uint32_t* scratch_n_of(mpcd_ctx* c) { return c->small + 6; }
+uint32_t* placed_of(mpcd_ctx* c) { return c->small + 7; }
 
 struct DeviceGuard {
   int prev = -1;
@@ -322,7 +429,38 @@ PlaceArgs place_args(mpcd_ctx* c, int b, int64_t step) {
   P.a = g.cell_size;
   P.unit = g.cell_size == 1.0;
   P.L0 = g.dims[0]; P.L1 = g.dims[1]; P.L2 = g.dims[2];
+  P.multi = c->multi ? 1 : 0;
+  P.strict = 0;
+  P.G0 = c->multi ? c->dom.global_dims[0] : g.dims[0];
+  P.G1 = c->multi ? c->dom.global_dims[1] : g.dims[1];
+  P.G2 = c->multi ? c->dom.global_dims[2] : g.dims[2];
+  P.org0 = c->org[0]; P.org1 = c->org[1]; P.org2 = c->org[2];
   return P;
+}
+
+// Device-usable address of a caller buffer: pinned (page-locked, UVA-mapped)
+// host memory and device memory are read / written by the kernels in place;
+// pageable host memory gives nullptr (the caller stages it).
+template <class T>
+T* mapped(T* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type == cudaMemoryTypeHost && a.devicePointer) return static_cast<T*>(a.devicePointer);
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return p;
+  return nullptr;
+}
+
+// particles placed by the last filtered placement (multi-domain upload/init)
+int read_placed(mpcd_ctx* c, cudaStream_t st, int64_t* out) {
+  uint32_t h = 0;
+  MPCD_CUDA(cudaMemcpyAsync(&h, placed_of(c), 4, cudaMemcpyDeviceToHost, st));
+  MPCD_CUDA(cudaStreamSynchronize(st));
+  *out = h;
+  return MPCD_OK;
 }
 
 // Flatten the binned state of reg[cur] into rows of reg[cur ^ 1] (cell-major
@@ -360,7 +498,9 @@ int flatten(mpcd_ctx* c, bool by_id, cudaStream_t st) {
 int place_flat(mpcd_ctx* c, int64_t step, cudaStream_t st) {
   const int b = c->flat ^ 1;
   if (c->n > 0) {
-    k_place_flat<<<grid_for(c->n, 256), 256, 0, st>>>(c->reg[c->flat], c->n, place_args(c, b, step));
+    PlaceArgs P = place_args(c, b, step);
+    P.strict = 1;  // every resident particle is this domain's
+    k_place_flat<<<grid_for(c->n, 256), 256, 0, st>>>(c->reg[c->flat], c->n, P);
     MPCD_LAUNCH_CHECK();
   }
   c->cur = b;
@@ -383,9 +523,12 @@ int check_flags(mpcd_ctx* c, cudaStream_t st) {
   uint32_t fl[4];
   MPCD_CUDA(cudaMemcpyAsync(fl, flags_of(c), sizeof(fl), cudaMemcpyDeviceToHost, st));
   MPCD_CUDA(cudaStreamSynchronize(st));
-  if (fl[1] || fl[2]) {
-    cudaMemsetAsync(flags_of(c) + 1, 0, 2 * sizeof(uint32_t), st);
+  if (fl[1] || fl[2] || fl[3]) {
+    cudaMemsetAsync(flags_of(c) + 1, 0, 3 * sizeof(uint32_t), st);
     if (fl[1]) return fail(MPCD_ERR_RNG, "axis rejection sampling failed to terminate");
+    if (fl[3])
+      return fail(MPCD_ERR_TOPOLOGY, "a particle given to domain %d lies outside its cells",
+                  (int)c->dom.rank);
     return fail(MPCD_ERR_CAPACITY, "overflow list full: more particles in full cells than the "
                                    "context's overflow capacity %u", c->ovf_cap);
   }
@@ -436,6 +579,25 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.m0 = g.mass_value;
   A.part_base = 0;
   (void)by_id;
+  if (c->multi) {
+    A.G0 = (int)c->dom.global_dims[0]; A.G1 = (int)c->dom.global_dims[1];
+    A.G2 = (int)c->dom.global_dims[2];
+    A.o0 = (int)c->org[0]; A.o1 = (int)c->org[1]; A.o2 = (int)c->org[2];
+    A.R1 = c->dom.rank_dims[1]; A.R2 = c->dom.rank_dims[2];
+    A.box0 = (double)A.G0 * g.cell_size;
+    A.box1 = (double)A.G1 * g.cell_size;
+    A.box2 = (double)A.G2 * g.cell_size;
+    A.send = c->send;
+    A.send_n = c->send_n;
+    A.send_cap = (uint32_t)c->dom.send_capacity;
+  } else {
+    A.G0 = A.L0; A.G1 = A.L1; A.G2 = A.L2;
+    A.o0 = A.o1 = A.o2 = 0;
+    A.R1 = A.R2 = 1;
+    A.send = nullptr;
+    A.send_n = nullptr;
+    A.send_cap = 0;
+  }
   return A;
 }
 
@@ -462,10 +624,10 @@ constexpr int64_t kDenseGrid = 592;
 
 // which == 0: the persistent tile kernel (returns its grid); which == 1: the
 // dense-tile kernel after sorting its tile list.
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
+template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
 int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_t st) {
   if (which == 0) {
-    auto kern = k_step<UNIT, UMASS, DRIFT, COM, BYID>;
+    auto kern = k_step<UNIT, UMASS, DRIFT, COM, MODE>;
     const size_t smem = sizeof(StepSmem<DRIFT>);
     const int64_t grid =
         std::max<int64_t>(1, std::min<int64_t>(ntiles, resident_ctas((const void*)kern, kNTW, smem)));
@@ -473,23 +635,25 @@ int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_
     return grid;
   }
   k_sort_dense<<<1, 1, 0, st>>>(A.dense, A.flags);
-  k_step_dense<UNIT, UMASS, DRIFT, COM, BYID><<<(unsigned)kDenseGrid, kNT, 0, st>>>(A);
+  k_step_dense<UNIT, UMASS, DRIFT, COM, MODE><<<(unsigned)kDenseGrid, kNT, 0, st>>>(A);
   return kDenseGrid;
 }
 
-// 32 compile-time variants, chosen at run time
+// 48 compile-time variants, chosen at run time
 struct Variant {
-  bool unit, umass, drift, com, by_id;
+  bool unit, umass, drift, com;
+  int mode;
 };
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM>
-int64_t launch_byid(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.by_id) return launch_variant<UNIT, UMASS, DRIFT, COM, true>(A, nt, which, st);
-  return launch_variant<UNIT, UMASS, DRIFT, COM, false>(A, nt, which, st);
+int64_t launch_mode(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
+  if (v.mode == kById) return launch_variant<UNIT, UMASS, DRIFT, COM, kById>(A, nt, which, st);
+  if (v.mode == kMulti) return launch_variant<UNIT, UMASS, DRIFT, COM, kMulti>(A, nt, which, st);
+  return launch_variant<UNIT, UMASS, DRIFT, COM, kBinned>(A, nt, which, st);
 }
 template <bool UNIT, bool UMASS, bool DRIFT>
 int64_t launch_com(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.com) return launch_byid<UNIT, UMASS, DRIFT, true>(A, nt, v, which, st);
-  return launch_byid<UNIT, UMASS, DRIFT, false>(A, nt, v, which, st);
+  if (v.com) return launch_mode<UNIT, UMASS, DRIFT, true>(A, nt, v, which, st);
+  return launch_mode<UNIT, UMASS, DRIFT, false>(A, nt, v, which, st);
 }
 template <bool UNIT, bool UMASS>
 int64_t launch_drift(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
@@ -506,6 +670,10 @@ int64_t launch_step_kernel(const StepArgs& A, int64_t nt, Variant v, int which, 
 }
 
 int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t st) {
+  if (c->multi && !(c->binned && c->cur_step == step))
+    return fail(MPCD_ERR_CONFIG, "a decomposed domain steps consecutively: it holds the "
+                "particles of step %lld's cells, not of step %lld's",
+                (long long)c->cur_step, (long long)step);
   int rc = ensure_binned(c, step, st);
   if (rc) return rc;
   const bool com = (flags & MPCD_STEP_WANT_COM) != 0;
@@ -520,7 +688,8 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
     MPCD_CUDA(cudaEventRecord(ev[0], st));
   }
   const Variant v{c->cfg.cell_size == 1.0, c->cfg.uniform_mass != 0,
-                  (flags & MPCD_STEP_WANT_DRIFT) != 0, com, by_id};
+                  (flags & MPCD_STEP_WANT_DRIFT) != 0, com,
+                  by_id ? kById : (c->multi ? kMulti : kBinned)};
   const int64_t grid = launch_step_kernel(A, c->ntiles, v, 0, st);
   MPCD_LAUNCH_CHECK();
   if (ev) MPCD_CUDA(cudaEventRecord(ev[1], st));
@@ -548,6 +717,86 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
   return MPCD_OK;
 }
 
+int download_rows(mpcd_ctx* c, double* pos, double* vel, double* mass, int64_t* ids,
+                  int32_t id_order, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = c->n;
+  if (n == 0) return MPCD_OK;
+  Recs rows;
+  Recs tmp_recs;
+  void* tmp_slab = nullptr;
+  if (c->binned) {
+    // flatten into a scratch record array (the state stays binned)
+    MPCD_CUDA(cudaMallocAsync(&tmp_slab, (size_t)n * 64, st));
+    tmp_recs = carve(tmp_slab, n);
+    const int b = c->cur;
+    uint32_t h_ovf = 0;
+    MPCD_CUDA(cudaMemcpyAsync(&h_ovf, ovf_n_of(c, b), 4, cudaMemcpyDeviceToHost, st));
+    MPCD_CUDA(cudaStreamSynchronize(st));
+    const uint32_t n_ovf = std::min(h_ovf, c->ovf_cap);
+    uint32_t* offs = nullptr;
+    if (!id_order) {
+      MPCD_CUDA(cudaMallocAsync(&offs, sizeof(uint32_t) * 2 * c->C, st));
+      k_clamp_counts<<<grid_for(c->C, 256), 256, 0, st>>>(c->count[b], c->C, c->cap, offs + c->C);
+      int rc = scan_u32(c->scan, offs + c->C, offs, nullptr, c->C, false, st);
+      if (rc) return rc;
+    }
+    const int64_t work = c->C * (int64_t)c->cap + n_ovf;
+    k_flatten<<<grid_for(work, 256), 256, 0, st>>>(c->reg[b], c->count[b], c->C, c->cap, offs,
+                                                   c->ovf[b], n_ovf, (uint32_t)(n - n_ovf),
+                                                   id_order ? 1 : 0, tmp_recs);
+    MPCD_LAUNCH_CHECK();
+    if (offs) MPCD_CUDA(cudaFreeAsync(offs, st));
+    rows = tmp_recs;
+  } else {
+    rows = c->reg[c->flat];  // flat rows are in id order already
+  }
+  double* tmp = nullptr;
+  MPCD_CUDA(cudaMallocAsync(&tmp, (size_t)n * 8 * 8, st));
+  double* dpos = tmp;
+  double* dvel = tmp + 3 * n;
+  double* dmass = tmp + 6 * n;
+  int64_t* dids = reinterpret_cast<int64_t*>(tmp + 7 * n);
+  k_flat_to_rows<<<grid_for(n, 256), 256, 0, st>>>(rows, n, pos ? dpos : nullptr,
+                                                   vel ? dvel : nullptr, mass ? dmass : nullptr,
+                                                   ids ? dids : nullptr, c->cfg.uniform_mass,
+                                                   c->cfg.mass_value);
+  MPCD_LAUNCH_CHECK();
+  if (pos) MPCD_CUDA(cudaMemcpyAsync(pos, dpos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+  if (vel) MPCD_CUDA(cudaMemcpyAsync(vel, dvel, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+  if (mass) MPCD_CUDA(cudaMemcpyAsync(mass, dmass, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  if (ids) MPCD_CUDA(cudaMemcpyAsync(ids, dids, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+  MPCD_CUDA(cudaFreeAsync(tmp, st));
+  if (tmp_slab) MPCD_CUDA(cudaFreeAsync(tmp_slab, st));
+  MPCD_CUDA(cudaStreamSynchronize(st));
+  return MPCD_OK;
+}
+
+
+// Multi-domain download: storage order, then rows sorted by (global) id on
+// the host when id_order is asked for.
+int download_multi(mpcd_ctx* c, double* pos, double* vel, double* mass, int64_t* ids,
+                   int32_t id_order, void* stream) {
+  const int64_t n = c->n;
+  std::vector<double> hp(3 * n), hv(3 * n), hm(n);
+  std::vector<int64_t> hi(n);
+  int rc = download_rows(c, hp.data(), hv.data(), hm.data(), hi.data(), 0, stream);
+  if (rc) return rc;
+  std::vector<int64_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  if (id_order)
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return hi[a] < hi[b]; });
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t i = order[r];
+    if (pos) for (int d = 0; d < 3; ++d) pos[3 * r + d] = hp[3 * i + d];
+    if (vel) for (int d = 0; d < 3; ++d) vel[3 * r + d] = hv[3 * i + d];
+    if (mass) mass[r] = hm[i];
+    if (ids) ids[r] = hi[i];
+  }
+  return MPCD_OK;
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -565,6 +814,14 @@ int mpcd_ctx_create(const mpcd_config* cfg, mpcd_ctx** out) {
     return fail(MPCD_ERR_CONFIG, "capacity must be in [0, 2^32-1)");
   if (cfg->prng < 0 || cfg->prng > 3) return fail(MPCD_ERR_CONFIG, "unknown prng %d", cfg->prng);
   DeviceGuard dg(cfg->device);
+  {  // staging buffers of upload/download come from the stream-ordered pool:
+     // keep what is freed instead of returning it to the OS at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   mpcd_ctx* c = new mpcd_ctx();
   c->cfg = *cfg;
   c->dev = cfg->device;
@@ -630,6 +887,8 @@ int mpcd_ctx_destroy(mpcd_ctx* c) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : c->prof_events) cudaEventDestroy(e);
+  if (c->send) cudaFree(c->send);
+  if (c->send_n) cudaFree(c->send_n);
   c->scan.release();
   delete c;
   return MPCD_OK;
@@ -643,7 +902,7 @@ int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double*
                 const int64_t* ids, int64_t n, int64_t step, void* stream) {
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
-  if (n < 0 || n > c->cfg.capacity)
+  if (n < 0 || (!c->multi && n > c->cfg.capacity) || n >= (1LL << 32))
     return fail(MPCD_ERR_CAPACITY, "%lld particles exceed capacity %lld", (long long)n,
                 (long long)c->cfg.capacity);
   if (n > 0 && (!pos || !vel)) return fail(MPCD_ERR_CONFIG, "positions/velocities required");
@@ -657,7 +916,18 @@ int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double*
   }
   c->n = n;
   const int b = 0;
-  if (n > 0) {
+  if (c->multi) MPCD_CUDA(cudaMemsetAsync(placed_of(c), 0, 4, st));
+  const double* zpos = mapped(pos);
+  const double* zvel = mapped(vel);
+  const double* zmass = c->cfg.uniform_mass ? nullptr : mapped(mass);
+  const int64_t* zids = mapped(ids);
+  if (n > 0 && zpos && zvel && (c->cfg.uniform_mass || zmass) && (!ids || zids)) {
+    // pinned host (or device) rows: bin them straight from the caller's buffers
+    k_place_rows<<<grid_for(n, kRowBlock), kRowBlock, 0, st>>>(
+        zpos, zvel, zmass, zids, n, c->cfg.mass_value, place_args(c, b, step),
+        c->multi ? placed_of(c) : nullptr);
+    MPCD_LAUNCH_CHECK();
+  } else if (n > 0) {
     double* tmp = nullptr;
     const size_t bytes = (size_t)n * 8 * (3 + 3 + 1 + 1);
     MPCD_CUDA(cudaMallocAsync(&tmp, bytes, st));
@@ -670,11 +940,18 @@ int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double*
     if (!c->cfg.uniform_mass)
       MPCD_CUDA(cudaMemcpyAsync(dmass, mass, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     if (ids) MPCD_CUDA(cudaMemcpyAsync(dids, ids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
-    k_place_rows<<<grid_for(n, 256), 256, 0, st>>>(
+    k_place_rows<<<grid_for(n, kRowBlock), kRowBlock, 0, st>>>(
         dpos, dvel, c->cfg.uniform_mass ? nullptr : dmass, ids ? dids : nullptr, n,
-        c->cfg.mass_value, place_args(c, b, step));
+        c->cfg.mass_value, place_args(c, b, step), c->multi ? placed_of(c) : nullptr);
     MPCD_LAUNCH_CHECK();
     MPCD_CUDA(cudaFreeAsync(tmp, st));
+  }
+  if (c->multi) {  // the rows of other domains were dropped
+    int rc = read_placed(c, st, &c->n);
+    if (rc) return rc;
+    if (c->n > c->cfg.capacity)
+      return fail(MPCD_ERR_CAPACITY, "domain %d holds %lld particles, capacity %lld",
+                  (int)c->dom.rank, (long long)c->n, (long long)c->cfg.capacity);
   }
   c->cur = b;
   c->binned = true;
@@ -689,57 +966,8 @@ int mpcd_download(mpcd_ctx* c, double* pos, double* vel, double* mass, int64_t* 
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
   DeviceGuard dg(c->dev);
-  cudaStream_t st = as_stream(stream);
-  const int64_t n = c->n;
-  if (n == 0) return MPCD_OK;
-  Recs rows;
-  Recs tmp_recs;
-  void* tmp_slab = nullptr;
-  if (c->binned) {
-    // flatten into a scratch record array (the state stays binned)
-    MPCD_CUDA(cudaMallocAsync(&tmp_slab, (size_t)n * 64, st));
-    tmp_recs = carve(tmp_slab, n);
-    const int b = c->cur;
-    uint32_t h_ovf = 0;
-    MPCD_CUDA(cudaMemcpyAsync(&h_ovf, ovf_n_of(c, b), 4, cudaMemcpyDeviceToHost, st));
-    MPCD_CUDA(cudaStreamSynchronize(st));
-    const uint32_t n_ovf = std::min(h_ovf, c->ovf_cap);
-    uint32_t* offs = nullptr;
-    if (!id_order) {
-      MPCD_CUDA(cudaMallocAsync(&offs, sizeof(uint32_t) * 2 * c->C, st));
-      k_clamp_counts<<<grid_for(c->C, 256), 256, 0, st>>>(c->count[b], c->C, c->cap, offs + c->C);
-      int rc = scan_u32(c->scan, offs + c->C, offs, nullptr, c->C, false, st);
-      if (rc) return rc;
-    }
-    const int64_t work = c->C * (int64_t)c->cap + n_ovf;
-    k_flatten<<<grid_for(work, 256), 256, 0, st>>>(c->reg[b], c->count[b], c->C, c->cap, offs,
-                                                   c->ovf[b], n_ovf, (uint32_t)(n - n_ovf),
-                                                   id_order ? 1 : 0, tmp_recs);
-    MPCD_LAUNCH_CHECK();
-    if (offs) MPCD_CUDA(cudaFreeAsync(offs, st));
-    rows = tmp_recs;
-  } else {
-    rows = c->reg[c->flat];  // flat rows are in id order already
-  }
-  double* tmp = nullptr;
-  MPCD_CUDA(cudaMallocAsync(&tmp, (size_t)n * 8 * 8, st));
-  double* dpos = tmp;
-  double* dvel = tmp + 3 * n;
-  double* dmass = tmp + 6 * n;
-  int64_t* dids = reinterpret_cast<int64_t*>(tmp + 7 * n);
-  k_flat_to_rows<<<grid_for(n, 256), 256, 0, st>>>(rows, n, pos ? dpos : nullptr,
-                                                   vel ? dvel : nullptr, mass ? dmass : nullptr,
-                                                   ids ? dids : nullptr, c->cfg.uniform_mass,
-                                                   c->cfg.mass_value);
-  MPCD_LAUNCH_CHECK();
-  if (pos) MPCD_CUDA(cudaMemcpyAsync(pos, dpos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
-  if (vel) MPCD_CUDA(cudaMemcpyAsync(vel, dvel, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
-  if (mass) MPCD_CUDA(cudaMemcpyAsync(mass, dmass, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-  if (ids) MPCD_CUDA(cudaMemcpyAsync(ids, dids, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
-  MPCD_CUDA(cudaFreeAsync(tmp, st));
-  if (tmp_slab) MPCD_CUDA(cudaFreeAsync(tmp_slab, st));
-  MPCD_CUDA(cudaStreamSynchronize(st));
-  return MPCD_OK;
+  if (c->multi) return download_multi(c, pos, vel, mass, ids, id_order, stream);
+  return download_rows(c, pos, vel, mass, ids, id_order, stream);
 }
 
 int mpcd_step(mpcd_ctx* c, int64_t step, int32_t flags, void* stream) {
@@ -753,6 +981,9 @@ int mpcd_step(mpcd_ctx* c, int64_t step, int32_t flags, void* stream) {
 int mpcd_run(mpcd_ctx* c, int64_t first_step, int64_t n_steps, int32_t flags, void* stream) {
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
+  if (c->multi && n_steps > 1)
+    return fail(MPCD_ERR_CONFIG, "a decomposed domain exchanges leavers between steps: use "
+                                 "mpcd_step + mpcd_absorb");
   DeviceGuard dg(c->dev);
   for (int64_t k = 0; k < n_steps; ++k) {
     int rc = launch_step(c, first_step + k, flags, false, as_stream(stream));
@@ -790,13 +1021,22 @@ int mpcd_read_com(mpcd_ctx* c, int64_t* cell_ids, double* com, int64_t* n_occupi
   MPCD_CUDA(cudaMemcpyAsync(cx.data(), c->com_cap, sizeof(double) * 4 * c->C,
                             cudaMemcpyDeviceToHost, st));
   MPCD_CUDA(cudaStreamSynchronize(st));
-  int64_t k = 0;
+  // (global cell id, local cell) of the occupied cells, ascending by global id
+  std::vector<std::pair<int64_t, int64_t>> occ;
+  const int64_t* L = c->cfg.dims;
+  const int64_t* G = c->multi ? c->dom.global_dims : c->cfg.dims;
   for (int64_t cc = 0; cc < c->C; ++cc) {
     if (cx[4 * cc + 3] > 0.0) {
-      if (cell_ids) cell_ids[k] = cc;
-      if (com) for (int d = 0; d < 3; ++d) com[3 * k + d] = cx[4 * cc + d];
-      ++k;
+      const int64_t lz = cc % L[2], ly = (cc / L[2]) % L[1], lx = cc / (L[1] * L[2]);
+      const int64_t g = ((lx + c->org[0]) * G[1] + (ly + c->org[1])) * G[2] + (lz + c->org[2]);
+      occ.emplace_back(g, cc);
     }
+  }
+  if (c->multi) std::sort(occ.begin(), occ.end());
+  const int64_t k = (int64_t)occ.size();
+  for (int64_t j = 0; j < k; ++j) {
+    if (cell_ids) cell_ids[j] = occ[j].first;
+    if (com) for (int d = 0; d < 3; ++d) com[3 * j + d] = cx[4 * occ[j].second + d];
   }
   *n_occupied = k;
   return MPCD_OK;
@@ -806,6 +1046,7 @@ int mpcd_read_binning(mpcd_ctx* c, int64_t* cells, int64_t* bin_count, int64_t* 
                       int64_t* permutation, void* stream) {
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
+  if (c->multi) return fail(MPCD_ERR_CONFIG, "read_binning is for a whole-box context");
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
   int rc = ensure_binned(c, c->cur_step, st);
@@ -846,17 +1087,24 @@ int mpcd_step_host(mpcd_ctx* c, double* pos, double* vel, const double* mass, in
                    int64_t step, int32_t flags, double* drift, void* stream) {
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
+  if (c->multi) return fail(MPCD_ERR_CONFIG, "step_host is for a whole-box context");
   int rc = mpcd_upload(c, pos, vel, mass, nullptr, n, step, stream);
   if (rc) return rc;
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
   rc = launch_step(c, step, flags, true, st);
   if (rc) return rc;
-  if (n > 0) {  // by-id rows: row i == particle i
+  double* zpos = mapped(pos);
+  double* zvel = mapped(vel);
+  if (n > 0 && zpos && zvel) {  // by-id rows straight into the caller's pinned buffers
+    k_flat_to_rows_chunked<<<grid_for(n, kRowBlock), kRowBlock, 0, st>>>(c->reg[c->flat], n,
+                                                                         zpos, zvel);
+    MPCD_LAUNCH_CHECK();
+  } else if (n > 0) {  // by-id rows: row i == particle i
     double* tmp = nullptr;
     MPCD_CUDA(cudaMallocAsync(&tmp, sizeof(double) * 6 * n, st));
-    k_flat_to_rows<<<grid_for(n, 256), 256, 0, st>>>(c->reg[c->flat], n, tmp, tmp + 3 * n,
-                                                     nullptr, nullptr, 1, 0.0);
+    k_flat_to_rows_chunked<<<grid_for(n, kRowBlock), kRowBlock, 0, st>>>(c->reg[c->flat], n, tmp,
+                                                                         tmp + 3 * n);
     MPCD_LAUNCH_CHECK();
     MPCD_CUDA(cudaMemcpyAsync(pos, tmp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
     MPCD_CUDA(cudaMemcpyAsync(vel, tmp + 3 * n, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
@@ -872,7 +1120,8 @@ int mpcd_step_host(mpcd_ctx* c, double* pos, double* vel, const double* mass, in
 int mpcd_init_device(mpcd_ctx* c, int64_t n, double velocity_variance, int64_t step, void* stream) {
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
-  if (n < 0 || n > c->cfg.capacity) return fail(MPCD_ERR_CAPACITY, "n exceeds capacity");
+  if (n < 0 || (!c->multi && n > c->cfg.capacity) || n >= (1LL << 32))
+    return fail(MPCD_ERR_CAPACITY, "n exceeds capacity");
   if (!c->cfg.uniform_mass) return fail(MPCD_ERR_CONFIG, "device init needs uniform_mass");
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
@@ -880,27 +1129,114 @@ int mpcd_init_device(mpcd_ctx* c, int64_t n, double velocity_variance, int64_t s
     MPCD_CUDA(cudaMemsetAsync(c->count[b], 0, sizeof(uint32_t) * c->C, st));
     MPCD_CUDA(cudaMemsetAsync(ovf_n_of(c, b), 0, 4, st));
   }
-  c->n = n;
-  c->flat = 1;
-  c->binned = false;
+  MPCD_CUDA(cudaMemsetAsync(placed_of(c), 0, 4, st));
+  const int b = 0;
   if (n > 0) {
-    const int blocks = 148 * 8;
     double* part = nullptr;
-    MPCD_CUDA(cudaMallocAsync(&part, sizeof(double) * 3 * blocks, st));
+    MPCD_CUDA(cudaMallocAsync(&part, sizeof(double) * 3 * kInitBlocks, st));
     const mpcd_config& g = c->cfg;
-    k_init_device<<<blocks, 256, 0, st>>>(c->reg[1], n, key_state(g.seed, 0, kInit, 0),
-                                          g.dims[0] * g.cell_size, g.dims[1] * g.cell_size,
-                                          g.dims[2] * g.cell_size, sqrt(velocity_variance),
-                                          g.mass_value, part);
+    const int64_t* G = c->multi ? c->dom.global_dims : g.dims;
+    const uint64_t state = key_state(g.seed, 0, kInit, 0);
+    const double sigma = sqrt(velocity_variance);
+    k_init_sum<<<kInitBlocks, 256, 0, st>>>(n, state, sigma, part);
     MPCD_LAUNCH_CHECK();
-    k_init_remove_mean<<<blocks, 256, 0, st>>>(c->reg[1], n, part, blocks);
+    k_init_place<<<kInitBlocks, 256, 0, st>>>(n, state, G[0] * g.cell_size, G[1] * g.cell_size,
+                                              G[2] * g.cell_size, sigma, g.mass_value, part,
+                                              kInitBlocks, place_args(c, b, step), placed_of(c));
     MPCD_LAUNCH_CHECK();
     MPCD_CUDA(cudaFreeAsync(part, st));
   }
-  c->have_diag = false;
-  int rc = place_flat(c, step, st);
+  int rc = read_placed(c, st, &c->n);
   if (rc) return rc;
+  if (c->n > c->cfg.capacity)
+    return fail(MPCD_ERR_CAPACITY, "domain holds %lld particles, capacity %lld",
+                (long long)c->n, (long long)c->cfg.capacity);
+  c->cur = b;
+  c->binned = true;
+  c->flat = -1;
+  c->cur_step = step;
+  c->have_diag = false;
   return check_flags(c, st);
+}
+
+int mpcd_ctx_set_domain(mpcd_ctx* c, const mpcd_domain* dom) {
+  clear_error();
+  if (!c || !dom) return fail(MPCD_ERR_CONFIG, "null argument");
+  int64_t P = 1;
+  for (int d = 0; d < 3; ++d) {
+    if (dom->rank_dims[d] < 1) return fail(MPCD_ERR_TOPOLOGY, "rank_dims must be positive");
+    if (dom->global_dims[d] != c->cfg.dims[d] * dom->rank_dims[d])
+      return fail(MPCD_ERR_TOPOLOGY,
+                  "global_dims[%d] = %lld is not rank_dims * the context's dims (%lld * %d)", d,
+                  (long long)dom->global_dims[d], (long long)c->cfg.dims[d], dom->rank_dims[d]);
+    if (dom->global_dims[d] >= (1LL << 31)) return fail(MPCD_ERR_CONFIG, "global dims too large");
+    P *= dom->rank_dims[d];
+  }
+  if (dom->rank < 0 || dom->rank >= P) return fail(MPCD_ERR_TOPOLOGY, "rank out of range");
+  DeviceGuard dg(c->dev);
+  if (c->send) cudaFree(c->send);
+  if (c->send_n) cudaFree(c->send_n);
+  c->send = nullptr;
+  c->send_n = nullptr;
+  c->dom = *dom;
+  const int r = dom->rank;
+  const int bz = r % dom->rank_dims[2], by = (r / dom->rank_dims[2]) % dom->rank_dims[1];
+  const int bx = r / (dom->rank_dims[1] * dom->rank_dims[2]);
+  c->org[0] = bx * c->cfg.dims[0];
+  c->org[1] = by * c->cfg.dims[1];
+  c->org[2] = bz * c->cfg.dims[2];
+  int64_t cap = dom->send_capacity;
+  if (cap <= 0) cap = std::max<int64_t>(1 << 16, c->cfg.capacity / 16);
+  if (cap >= (1LL << 32)) cap = (1LL << 32) - 1;
+  c->dom.send_capacity = cap;
+  if (cudaMalloc(&c->send, (size_t)P * cap * sizeof(XRec)) != cudaSuccess ||
+      cudaMalloc(&c->send_n, sizeof(unsigned long long) * P) != cudaSuccess)
+    return fail(MPCD_ERR_CUDA, "cudaMalloc of %lld send records failed", (long long)(P * cap));
+  MPCD_CUDA(cudaMemset(c->send_n, 0, sizeof(unsigned long long) * P));
+  c->multi = true;
+  c->n = 0;
+  c->binned = false;
+  c->flat = -1;
+  c->have_diag = false;
+  MPCD_CUDA(cudaDeviceSynchronize());
+  return MPCD_OK;
+}
+
+int mpcd_exchange_buffers(mpcd_ctx* c, mpcd_exchange* out) {
+  clear_error();
+  if (!c || !out) return fail(MPCD_ERR_CONFIG, "null argument");
+  if (!c->multi) return fail(MPCD_ERR_CONFIG, "not a decomposed domain (mpcd_ctx_set_domain)");
+  out->send = c->send;
+  out->send_n = c->send_n;
+  out->send_capacity = c->dom.send_capacity;
+  out->n_ranks = c->dom.rank_dims[0] * c->dom.rank_dims[1] * c->dom.rank_dims[2];
+  out->record_bytes = (int32_t)sizeof(XRec);
+  return MPCD_OK;
+}
+
+int mpcd_absorb(mpcd_ctx* c, const void* recs, int64_t n_recv, int64_t n_sent, void* stream) {
+  clear_error();
+  if (!c) return fail(MPCD_ERR_CONFIG, "null context");
+  if (!c->multi) return fail(MPCD_ERR_CONFIG, "not a decomposed domain (mpcd_ctx_set_domain)");
+  if (!c->binned) return fail(MPCD_ERR_CONFIG, "absorb follows mpcd_step");
+  if (n_recv < 0 || n_sent < 0 || n_sent > c->n || (n_recv > 0 && !recs))
+    return fail(MPCD_ERR_CONFIG, "bad absorb counts");
+  if (c->n - n_sent + n_recv > c->cfg.capacity)
+    return fail(MPCD_ERR_CAPACITY, "domain %d would hold %lld particles, capacity %lld",
+                (int)c->dom.rank, (long long)(c->n - n_sent + n_recv),
+                (long long)c->cfg.capacity);
+  DeviceGuard dg(c->dev);
+  cudaStream_t st = as_stream(stream);
+  if (n_recv > 0) {
+    PlaceArgs P = place_args(c, c->cur, c->cur_step);
+    P.strict = 1;
+    k_place_xrecs<<<grid_for(n_recv, 256), 256, 0, st>>>(static_cast<const XRec*>(recs), n_recv, P);
+    MPCD_LAUNCH_CHECK();
+  }
+  const int64_t P = c->dom.rank_dims[0] * c->dom.rank_dims[1] * c->dom.rank_dims[2];
+  MPCD_CUDA(cudaMemsetAsync(c->send_n, 0, sizeof(unsigned long long) * P, st));
+  c->n += n_recv - n_sent;
+  return MPCD_OK;
 }
 
 int mpcd_profile(mpcd_ctx* c, int32_t enable) {

@@ -14,8 +14,10 @@
 // Compile-time specialisation: UNIT (cell_size == 1: (x - off)/a is exact
 // without the division), UMASS (uniform mass, the record's mass slot is
 // unused), DRIFT (capture_drift: per-cell post-collision moments in numpy
-// order), COM (capture_com: com rows to HBM), BYID (pure-function mode:
-// write row `id` of a flat array, no next binning).
+// order), COM (capture_com: com rows to HBM), MODE: kBinned (one domain),
+// kById (pure-function mode: write row `id` of a flat array, no next
+// binning) or kMulti (one domain of a decomposed box: leavers are written to
+// per-rank send buffers instead of a local cell).
 #pragma once
 
 namespace mpcd {
@@ -32,6 +34,11 @@ struct __align__(16) VRec {
 struct Recs {
   PRec* p;
   VRec* v;
+};
+// A particle bound for another domain: both records back to back (64 B)
+struct __align__(16) XRec {
+  PRec p;
+  VRec v;
 };
 
 __device__ __forceinline__ double id_bits(uint32_t id) {
@@ -86,7 +93,30 @@ struct StepArgs {
   int prng;
   double m0;
   int64_t part_base;          // first partials row of the dense kernel's CTAs
+  // multi-domain (MODE == kMulti): this context owns the cells [o, o + L) of
+  // a global G0 x G1 x G2 grid split into uniform blocks; rank of a block =
+  // (bx * R1 + by) * R2 + bz.  Leavers go to send[dest * send_cap + slot].
+  int G0, G1, G2;
+  int o0, o1, o2;
+  int R1, R2;
+  XRec* send;
+  unsigned long long* send_n;  // claimed per destination (may exceed send_cap)
+  uint32_t send_cap;
 };
+
+// Step kernel modes: binned single domain, by-id pure function, multi-domain
+constexpr int kBinned = 0, kById = 1, kMulti = 2;
+
+// Global (whole-box) id of local cell c: the key of its rotation axis
+// (engine.py:82-92, 225-227 key axes by the global cell id).
+template <int MODE>
+__device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c) {
+  if (MODE != kMulti) return (uint64_t)c;
+  const int64_t lz = c % A.L2, t = c / A.L2;
+  const int64_t ly = t % A.L1, lx = t / A.L1;
+  return ((uint64_t)(lx + A.o0) * (uint64_t)A.G1 + (uint64_t)(ly + A.o1)) * (uint64_t)A.G2 +
+         (uint64_t)(lz + A.o2);
+}
 
 #ifndef MPCD_TC
 #define MPCD_TC 16
@@ -128,6 +158,25 @@ __device__ __forceinline__ uint32_t next_cell(const StepArgs& A, double x, doubl
   const unsigned iy = cell_coord32<UNIT>(y, A.off_next1, A.a, A.L1);
   const unsigned iz = cell_coord32<UNIT>(z, A.off_next2, A.a, A.L2);
   return (ix * (unsigned)A.L1 + iy) * (unsigned)A.L2 + iz;
+}
+
+// Multi-domain: the next-step cell in global coordinates (the serial
+// formula, so binning is bit-identical to one domain); true and the local
+// key when this domain owns it, else false and the owning rank.
+template <bool UNIT>
+__device__ __forceinline__ bool next_cell_multi(const StepArgs& A, double x, double y, double z,
+                                                uint32_t& key, int& dest) {
+  const int gx = cell_coord32<UNIT>(x, A.off_next0, A.a, A.G0);
+  const int gy = cell_coord32<UNIT>(y, A.off_next1, A.a, A.G1);
+  const int gz = cell_coord32<UNIT>(z, A.off_next2, A.a, A.G2);
+  const unsigned lx = (unsigned)(gx - A.o0), ly = (unsigned)(gy - A.o1), lz = (unsigned)(gz - A.o2);
+  if (lx < (unsigned)A.L0 && ly < (unsigned)A.L1 && lz < (unsigned)A.L2) {
+    key = (lx * (unsigned)A.L1 + ly) * (unsigned)A.L2 + lz;
+    return true;
+  }
+  dest = ((gx / A.L0) * A.R1 + gy / A.L1) * A.R2 + gz / A.L2;
+  key = 0u;
+  return false;
 }
 
 __device__ __noinline__ double wrap_slow(double x, double box) { return wrap(x, box); }
@@ -223,20 +272,51 @@ __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, uns
   }
 }
 
+// Multi-domain leavers: one atomic per destination rank per warp; a
+// destination's count may run past send_cap (the host sees it and fails).
+// Must be reached by the whole warp.
+__device__ __forceinline__ void send_foreign(const StepArgs& A, bool active, int dest,
+                                             const double* o, uint32_t id, double m) {
+  const unsigned act = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned grp = __match_any_sync(act, dest);
+  const int leader = __ffs(grp) - 1;
+  unsigned long long base = 0ull;
+  if (lane == leader) base = atomicAdd(&A.send_n[dest], (unsigned long long)__popc(grp));
+  base = __shfl_sync(grp, base, leader);
+  const unsigned long long slot = base + (unsigned long long)__popc(grp & ((1u << lane) - 1u));
+  if (slot < A.send_cap) {
+    XRec* x = A.send + (uint64_t)dest * A.send_cap + slot;
+    st2(&x->p.x, o[0], o[1]);
+    st2(&x->p.z, o[2], id_bits(id));
+    st2(&x->v.vx, o[3], o[4]);
+    st2(&x->v.vz, o[5], m);
+  }
+}
+
 // Unbatched variant for the dense kernel.
-template <bool UNIT, bool BYID>
+template <bool UNIT, int MODE>
 __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, double ny,
                                      double nz, uint32_t id, const double* w, double m) {
   const double o[6] = {nx, ny, nz, w[0], w[1], w[2]};
-  if (BYID) {
+  if (MODE == kById) {
     if (active) store_rec(A.out, id, nx, ny, nz, id, w[0], w[1], w[2], m);
     return;
   }
-  const uint32_t key = active ? next_cell<UNIT>(A, nx, ny, nz) : 0u;
+  uint32_t key = 0u;
+  bool local = active;
+  if (MODE == kMulti) {
+    int dest = 0;
+    if (active) local = next_cell_multi<UNIT>(A, nx, ny, nz, key, dest);
+    send_foreign(A, active && !local, dest, o, id, m);
+  } else if (active) {
+    key = next_cell<UNIT>(A, nx, ny, nz);
+  }
   unsigned grp;
   uint32_t base;
-  claim_slot(A, active, key, grp, base);
-  if (active) finish_slot(A, key, grp, base, o, id, m);
+  claim_slot(A, local, key, grp, base);
+  if (local) finish_slot(A, key, grp, base, o, id, m);
 }
 
 // ------------------------------------------------------------ TMA helpers --
@@ -335,6 +415,7 @@ __device__ __forceinline__ uint32_t tile_count(const StepArgs& A, int64_t tl, in
 // Producer warp: lay out tile `tl` in `B` from its counts (one per lane),
 // start its copies, draw its axes.  Completes two arrivals on `full` (one
 // with the byte count, one once the generic writes are done).
+template <int MODE>
 __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint64_t* full,
                                              int64_t tl, int64_t ntiles, uint32_t cnt,
                                              uint64_t pol) {
@@ -390,15 +471,16 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane < kTC) {
     double* ax = B.ax + lane * 3;
     ax[0] = ax[1] = ax[2] = 0.0;
-    if (cnt > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, (uint64_t)(c0 + lane), ax))
+    if (cnt > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, global_cell_id<MODE>(A, c0 + lane), ax))
       atomicOr(&A.flags[1], 1u);
   }
   __syncwarp();
   if (lane == 0) mbar_arrive(full);  // release: layout, table and axes written
 }
 
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
+template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
 __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int64_t ntiles) {
+  constexpr bool BYID = MODE == kById;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -420,7 +502,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
       const int b = (int)(i & 1);
       const uint32_t cnt_next = tile_count(A, tile + G, ntiles);  // in flight meanwhile
       if (i >= 2) mbar_wait(&S.empty[b], (uint32_t)((i >> 1) - 1) & 1u);
-      prepare_tile(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
+      prepare_tile<MODE>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
       cnt = cnt_next;
     }
     return;
@@ -517,9 +599,13 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     uint32_t key[kPPTT];
     double mm[kPPTT];
     uint32_t pid[kPPTT];
+    bool stay[kPPTT];  // kMulti: the next cell is this domain's
+    int dest[kPPTT];
 #pragma unroll
     for (int r = 0; r < kPPTT; ++r) {
       key[r] = 0u;
+      stay[r] = real[r];
+      dest[r] = 0;
       if (real[r]) {
         const int j = r * kNC + t;
         const PRec p = T.p[j];
@@ -534,7 +620,10 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
         o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
         pid[r] = p.id;
         mm[r] = UMASS ? A.m0 : vr.m;
-        key[r] = BYID ? p.id : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
+        if (MODE == kMulti)
+          stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]);
+        else
+          key[r] = BYID ? p.id : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
         const double m = mm[r];
         double2* sv = reinterpret_cast<double2*>(S.val + slot[r] * 4);
         sv[0] = make_double2(m * w[0], m * w[1]);
@@ -554,12 +643,17 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
       for (int r = 0; r < kPPTT; ++r) {
         grp[r] = 0u;
         base[r] = 0u;
-        if (r * kNC < npad)  // warp-uniform: every lane takes part in the ballot
-          claim_slot(A, real[r], key[r], grp[r], base[r]);
+        if (r * kNC < npad) {  // warp-uniform: every lane takes part in the ballot
+          if (MODE == kMulti)
+            send_foreign(A, real[r] && !stay[r], dest[r], o[r], pid[r], mm[r]);
+          claim_slot(A, stay[r], key[r], grp[r], base[r]);
+        }
       }
     }
     consumer_sync();
-    if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
+    // the tile buffer is free for the producer (DRIFT still reads its
+    // off/cnt below and releases it after that)
+    if (!DRIFT && lane == 0) mbar_arrive(&S.empty[b]);
 
     // phase 6: conservation sums over this thread's staged rows, in slot
     // order (fixed: deterministic) -- while the slot claims are in flight
@@ -575,7 +669,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     if (!BYID) {
 #pragma unroll
       for (int r = 0; r < kPPTT; ++r)
-        if (real[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
+        if (stay[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
     }
     if (DRIFT) {
       for (int task = t; task < nc * 4; task += kNC) {
@@ -583,6 +677,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
         S.post[task] = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
       }
       consumer_sync();
+      if (lane == 0) mbar_arrive(&S.empty[b]);
       if (warp == 1) {
         double worst = 0.0;
         for (int lc = lane; lc < nc; lc += 32)
@@ -615,7 +710,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 // cell's region slots plus its overflow entries into HBM staging, then the
 // same phases with plain loops; ranking is O(k^2) per cell.  One CTA per
 // queued tile (grid-strided); staging ranges come from a bump allocator.
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM, bool BYID>
+template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
 __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
   __shared__ uint32_t s_cnt[kTC];
   __shared__ uint32_t s_off[kTC + 1];
@@ -709,7 +804,7 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       double* cx = s_cx + t * 6;
       for (int d = 0; d < 3; ++d) cx[d] = (mass > 0.0) ? s_mom[t * 4 + d] / mass : 0.0;
       cx[3] = cx[4] = cx[5] = 0.0;
-      if (s_cnt[t] > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, (uint64_t)(c0 + t), cx + 3))
+      if (s_cnt[t] > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, global_cell_id<MODE>(A, c0 + t), cx + 3))
         atomicOr(&A.flags[1], 1u);
       if (COM) {
         double* g = A.com_cap + (c0 + t) * 4;
@@ -739,7 +834,7 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
         g_val[4 * s] = m * w[0]; g_val[4 * s + 1] = m * w[1]; g_val[4 * s + 2] = m * w[2];
         g_val[4 * s + 3] = m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]);
       }
-      emit<UNIT, BYID>(A, active, nx, ny, nz, id, w, UMASS ? A.m0 : m);
+      emit<UNIT, MODE>(A, active, nx, ny, nz, id, w, UMASS ? A.m0 : m);
     }
     __syncthreads();
     for (int task = t; task < nc * 4; task += kNT) {

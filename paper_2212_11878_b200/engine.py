@@ -9,6 +9,8 @@ backends registered in the same backend dispatch (engine.py:524-542):
   reference call sites run unmodified.
 * ``"nccl"`` -- slab/pencil domain decomposition over several GPUs, one
   process per GPU (see ``distributed.py``).
+* ``"sequential"`` -- the same decomposition with every domain in this
+  process on one GPU (the reference's in-process ``sequential`` backend).
 """
 
 from __future__ import annotations
@@ -28,7 +30,8 @@ from .particles import ParticleSet, init_system
 BACKEND_CUDA = "cuda"
 BACKEND_NCCL = "nccl"
 BACKEND_SERIAL = "serial"  # alias of "cuda" (the single-domain path)
-BACKENDS = (BACKEND_CUDA, BACKEND_NCCL, BACKEND_SERIAL)
+BACKEND_SEQUENTIAL = "sequential"  # decomposed box, every domain in this process
+BACKENDS = (BACKEND_CUDA, BACKEND_NCCL, BACKEND_SERIAL, BACKEND_SEQUENTIAL)
 POLICY_IMMEDIATE = "immediate"
 POLICY_LAZY = "lazy"
 POLICIES = (POLICY_IMMEDIATE, POLICY_LAZY)
@@ -142,6 +145,24 @@ class EngineContext:
             self.handle, cells.ctypes.data_as(_lib._i64), counts.ctypes.data_as(_lib._i64),
             offsets.ctypes.data_as(_lib._i64), perm.ctypes.data_as(_lib._i64), _dev.stream()))
         return cells, counts, offsets, perm
+
+    # ------------------------------------------------ decomposed box ---
+    def set_domain(self, global_dims, rank_dims, rank: int, send_capacity: int = 0):
+        dom = _lib.MpcdDomain()
+        for d in range(3):
+            dom.global_dims[d] = int(global_dims[d])
+            dom.rank_dims[d] = int(rank_dims[d])
+        dom.rank = int(rank)
+        dom.send_capacity = int(send_capacity)
+        _lib.check(self._lib.mpcd_ctx_set_domain(self.handle, C.byref(dom)))
+        ex = _lib.MpcdExchange()
+        _lib.check(self._lib.mpcd_exchange_buffers(self.handle, C.byref(ex)))
+        self.exchange_info = ex
+        return ex
+
+    def absorb(self, recv_ptr: int, n_recv: int, n_sent: int):
+        _lib.check(self._lib.mpcd_absorb(self.handle, C.c_void_p(int(recv_ptr) or None),
+                                         int(n_recv), int(n_sent), _dev.stream()))
 
     def step_host(self, positions, velocities, masses, step: int, want_drift: bool,
                   want_com: bool = False):
@@ -304,11 +325,12 @@ class Simulation:
             self._runner = CudaRunner(params, capture_drift=capture_drift,
                                       capture_com=capture_com,
                                       velocity_variance=velocity_variance, init=init)
-        elif backend == BACKEND_NCCL:
-            from .distributed import NcclRunner
-            self._runner = NcclRunner(params, policy=policy, capture_drift=capture_drift,
-                                      capture_com=capture_com,
-                                      velocity_variance=velocity_variance, init=init)
+        elif backend in (BACKEND_NCCL, BACKEND_SEQUENTIAL):
+            from .distributed import NcclRunner, SequentialRunner
+            cls = NcclRunner if backend == BACKEND_NCCL else SequentialRunner
+            self._runner = cls(params, policy=policy, capture_drift=capture_drift,
+                               capture_com=capture_com, velocity_variance=velocity_variance,
+                               init=init)
         else:
             raise ConfigError(f"unknown backend {backend!r}")
 

@@ -60,7 +60,8 @@ def test_no_fma_contraction_in_parity_kernels():
             if m:
                 entry = m.group(1)
             if "fma.rn.f64" in line:
-                assert entry is not None and "k_init_device" in entry, (path, entry)
+                assert entry is not None and ("k_init_sum" in entry or "k_init_place" in entry), \
+                    (path, entry)
 
 
 def test_host_rng_helpers_match_oracle(lib):

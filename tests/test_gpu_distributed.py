@@ -1,0 +1,157 @@
+"""GPU parity of the decomposed box: every domain layout
+must reproduce the whole-box engine bit for bit -- positions, velocities,
+com captures -- because a rank owns whole shifted cells and keys their axes
+by the global cell id.  Mirrors the reference's own parallel-vs-serial tests
+(test_engine.py:119-135: 1 rank bitwise == serial; N ranks within 1e-10),
+with the stronger bitwise bar.
+
+Run on a B200: python -m pytest tests -m gpu
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2212_11878_b200 as mp
+from paper_2212_11878_b200 import distributed as D
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run(params, backend, n_steps, **kw):
+    with mp.Simulation(params, backend=backend, **kw) as sim:
+        diags = [sim.step() for _ in range(n_steps)]
+        ids, p = sim.collect()
+        coms = list(sim.com_captures)
+        drift = list(sim.drift_history)
+    return ids, p, diags, coms, drift
+
+
+@pytest.mark.parametrize("dims,rank_dims", [
+    ((16, 16, 16), (2, 1, 1)),
+    ((16, 16, 16), (4, 1, 1)),
+    ((16, 16, 16), (2, 2, 1)),
+    ((16, 16, 16), (1, 2, 2)),
+    ((16, 16, 16), (2, 2, 2)),
+    ((24, 16, 8), (4, 2, 1)),   # non-cubic, pencil (the config-5 shape in small)
+])
+def test_sequential_domains_bitwise_equal_whole_box(dims, rank_dims):
+    base = mp.SimParams(edge_length=dims[0], edge_lengths=dims, seed=11)
+    dec = mp.SimParams(edge_length=dims[0], edge_lengths=dims, seed=11, rank_dims=rank_dims)
+    ids_a, pa, da, ca, _ = run(base, "cuda", 6, capture_com=True)
+    ids_b, pb, db, cb, _ = run(dec, "sequential", 6, capture_com=True)
+    assert np.array_equal(ids_a, ids_b)
+    assert np.array_equal(pa.positions, pb.positions)
+    assert np.array_equal(pa.velocities, pb.velocities)
+    for (ia, va), (ib, vb) in zip(ca, cb):
+        assert np.array_equal(ia, ib) and np.array_equal(va, vb)
+    for x, y in zip(da, db):
+        assert x["n"] == y["n"]
+        assert np.allclose(x["momentum"], y["momentum"], atol=1e-9)
+        assert abs(x["energy"] - y["energy"]) <= 1e-10 * x["energy"]
+        assert x["mass"] == y["mass"]
+    assert sum(d["crossings"] for d in db) > 0
+
+
+def test_one_domain_nccl_equals_cuda():
+    """test_engine.py:129-135: one rank of the parallel path == serial, bitwise."""
+    import torch.distributed as dist
+
+    params = mp.SimParams(edge_length=12, seed=2)
+    ids_a, pa, _, _, _ = run(params, "cuda", 5)
+    os.environ["MASTER_PORT"] = str(_free_port())
+    D.init_distributed("nccl")
+    try:
+        ids_b, pb, db, _, _ = run(params, "nccl", 5)
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(pa.positions, pb.positions)
+    assert np.array_equal(pa.velocities, pb.velocities)
+    assert all(d["crossings"] == 0 for d in db)
+
+
+@pytest.mark.parametrize("prng", ["splitmix", "pcg32"])
+def test_device_init_domains_equal_whole_box(prng):
+    dims = (32, 32, 32)
+    base = mp.SimParams(edge_length=32, seed=7, prng=prng)
+    dec = mp.SimParams(edge_length=32, seed=7, prng=prng, rank_dims=(4, 1, 1))
+    ids_a, pa, _, _, drift_a = run(base, "cuda", 4, init="device", capture_drift=True)
+    ids_b, pb, _, _, drift_b = run(dec, "sequential", 4, init="device", capture_drift=True)
+    assert np.array_equal(ids_a, ids_b)
+    assert np.array_equal(pa.positions, pb.positions)
+    assert np.array_equal(pa.velocities, pb.velocities)
+    assert np.allclose(drift_a, drift_b, rtol=0, atol=1e-12)
+    del dims
+
+
+def test_migration_overflow_raises():
+    params = mp.SimParams(edge_length=16, seed=1, rank_dims=(2, 1, 1))
+    from paper_2212_11878_b200.distributed import SequentialRunner
+    r = SequentialRunner(params, send_capacity=8)
+    try:
+        with pytest.raises(mp.MpcdError, match="overflow"):
+            r.run_step(0)
+    finally:
+        r.close()
+
+
+def test_domain_rejects_bad_topology():
+    from paper_2212_11878_b200.engine import EngineContext
+    ctx = EngineContext((8, 8, 8), 1.0, 0.1, 1.0, 0, "splitmix", 6000, mass_value=1.0)
+    try:
+        with pytest.raises(mp.TopologyError):
+            ctx.set_domain((24, 8, 8), (2, 1, 1), 0)  # 24 != 2 * 8
+        with pytest.raises(mp.TopologyError):
+            ctx.set_domain((16, 8, 8), (2, 1, 1), 2)  # rank out of range
+    finally:
+        ctx.close()
+
+
+# ------------------------------------- two processes on one GPU (gloo) ---
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        params = mp.SimParams(edge_length=16, seed=4, rank_dims=(world, 1, 1))
+        with mp.Simulation(params, backend="nccl", capture_com=True) as sim:
+            diags = [sim.step() for _ in range(4)]
+            ids, p = sim.collect()
+            ci, cv = sim.com_captures[-1]
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids, pos=p.positions,
+                 vel=p.velocities, ci=ci, cv=cv, crossings=[d["crossings"] for d in diags])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_gloo_equal_whole_box(tmp_path):
+    import torch.multiprocessing as tmp_mp
+
+    tmp_mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    params = mp.SimParams(edge_length=16, seed=4)
+    ids, p, _, coms, _ = run(params, "cuda", 4, capture_com=True)
+    for r in range(2):
+        o = np.load(tmp_path / f"r{r}.npz")
+        assert np.array_equal(o["ids"], ids)
+        assert np.array_equal(o["pos"], p.positions)
+        assert np.array_equal(o["vel"], p.velocities)
+        assert np.array_equal(o["ci"], coms[-1][0]) and np.array_equal(o["cv"], coms[-1][1])
+        assert np.all(o["crossings"] > 0)

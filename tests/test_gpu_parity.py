@@ -301,3 +301,34 @@ def test_advance_equals_step_loop():
     finally:
         a.close()
         b.close()
+
+
+def test_pure_step_pinned_buffers_equal_pageable():
+    """mpcd_step_host reads/writes pinned host rows in place (zero-copy) and
+    stages pageable ones: both must give the oracle's step bit for bit."""
+    import torch
+
+    params = mp.SimParams(edge_length=12, seed=21)
+    p = mp.init_system(params)
+    n = p.n
+    ctx = engine.EngineContext(params.dims, 1.0, params.dt, params.alpha, params.seed,
+                               "splitmix", n, mass_value=1.0)
+    try:
+        pos_t = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+        vel_t = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
+        pin_pos, pin_vel = pos_t.numpy(), vel_t.numpy()
+        pin_pos[:] = p.positions
+        pin_vel[:] = p.velocities
+        pag_pos, pag_vel = p.positions.copy(), p.velocities.copy()
+        ref_pos, ref_vel = p.positions, p.velocities
+        cs, sn = float(np.cos(params.alpha)), float(np.sin(params.alpha))
+        for k in range(3):
+            ctx.step_host(pin_pos, pin_vel, None, k, False)
+            ctx.step_host(pag_pos, pag_vel, None, k, False)
+            r = oracle.serial_step(ref_pos, ref_vel, np.ones(n), 12, 1.0, params.dt, cs, sn,
+                                   params.seed, k)
+            ref_pos, ref_vel = r.positions, r.velocities
+            assert np.array_equal(pin_pos, ref_pos) and np.array_equal(pin_vel, ref_vel)
+            assert np.array_equal(pag_pos, ref_pos) and np.array_equal(pag_vel, ref_vel)
+    finally:
+        ctx.close()
