@@ -121,9 +121,6 @@ __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c)
 #ifndef MPCD_TC
 #define MPCD_TC 16
 #endif
-#ifndef MPCD_NC
-#define MPCD_NC 128
-#endif
 #ifndef MPCD_MAXPT
 #define MPCD_MAXPT 256
 #endif
@@ -363,19 +360,28 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 // ------------------------------------------------------- the step kernel --
-// Persistent and warp-specialised.  CTA b walks tiles b, b + G, ...  Warp 8
-// (producer) prepares tiles ahead of the others: reads the tile's counts,
-// lays out its records in shared memory (each cell padded to a multiple of 4
-// slots), writes the slot -> cell table, issues one cp.async.bulk (TMA) per
-// cell and record array, zeroes the consumed counts and draws the cells'
-// rotation axes.  Warps 0-7 (consumers) collide the tile from shared memory
-// and write every particle into its next-step cell.  Two tile buffers with
-// full / empty mbarriers; the consumers synchronise among themselves with a
-// named barrier, never with the producer.
+// Persistent and warp-specialised.  CTA b walks tiles b, b + G, ...  The
+// producer warp prepares tiles ahead of the consumers: reads the tile's
+// counts, lays out its records in shared memory (each cell padded to a
+// multiple of 4 slots), writes the slot -> cell table, issues one
+// cp.async.bulk (TMA) per cell and record array, zeroes the consumed counts
+// and draws the cells' rotation axes.  Each consumer warp owns kCW = 4 cells
+// of the tile and runs every phase on them alone -- rank, moments, com,
+// rotation, stream, next-cell claims and stores -- synchronised only by
+// __syncwarp, in warp-private shared scratch; so consumer warps never wait
+// for each other.  Two tile buffers with full / empty mbarriers (empty
+// counts one arrival per consumer warp).
 constexpr int kMaxPT = MPCD_MAXPT;     // padded record slots per tile in shared memory
-constexpr int kNC = MPCD_NC;           // consumer threads
+constexpr int kCW = 4;                 // cells per consumer warp
+constexpr int kNCW = kTC / kCW;        // consumer warps
+constexpr int kNC = kNCW * 32;         // consumer threads
 constexpr int kNTW = kNC + 32;         // + one producer warp
-constexpr int kPPTT = kMaxPT / kNC;
+#ifndef MPCD_ROWSW
+#define MPCD_ROWSW 2
+#endif
+constexpr int kRowsW = MPCD_ROWSW;     // slot rows per consumer lane
+constexpr int kSlotsW = 32 * kRowsW;   // padded slots one consumer warp can hold
+static_assert(kTC % kCW == 0 && kTC <= 32, "tile = whole consumer warps, one producer lane per cell");
 
 struct TileBuf {
   PRec p[kMaxPT];
@@ -387,15 +393,22 @@ struct TileBuf {
   int skip;  // past the end, or a dense tile (queued for k_step_dense)
 };
 
+// Warp-private scratch.  Staged rows of cell q (0..3 inside the warp) live
+// at rows [lo_q + q, hi_q + q) of val: the one-row skew per cell puts the four
+// cells' moment columns in different bank groups.
+struct __align__(16) WarpScratch {
+  double val[(kSlotsW + kCW) * 4];  // (m v, m) rows in rank order; post rows later
+  uint32_t id[kSlotsW];             // ids in slot order, sentinel in padding
+  double mom[kCW * 4];
+  double com[kCW * 3];
+};
+
 template <bool DRIFT>
 struct StepSmem {
   TileBuf buf[2];
-  double val[kMaxPT * 4];  // staged rows in (cell, id) order; zero in padding
-  uint32_t id[kMaxPT];     // ids in slot order, sentinel in padding
-  double mom[kTC * 4];
+  WarpScratch w[kNCW];
   double post[DRIFT ? kTC * 4 : 1];
-  double com[kTC * 3];
-  double red[(kNC / 32) * 5];
+  double red[kNCW * 5];
   uint64_t full[2], empty[2];
 };
 
@@ -431,7 +444,8 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
     if (lane >= o) incl += y;
   }
   const uint32_t excl = incl - pad;
-  const bool over = __any_sync(0xffffffffu, cnt > A.cap);
+  // a consumer warp pass holds at most kSlotsW padded slots
+  const bool over = __any_sync(0xffffffffu, cnt > A.cap || pad > (uint32_t)kSlotsW);
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   const bool skip = tl >= ntiles || over || total > (uint32_t)kMaxPT;
   if (lane < kTC) {
@@ -478,9 +492,180 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane == 0) mbar_arrive(full);  // release: layout, table and axes written
 }
 
+// One consumer warp's cells of one tile: every phase, R slot rows per lane.
+template <int R, bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE, class Smem>
+__device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBuf& T,
+                                              WarpScratch& W, int64_t c0, int cw0,
+                                              int ncw, int j0, int j1, double* acc) {
+  constexpr bool BYID = MODE == kById;
+  const int lane = threadIdx.x & 31;
+
+  // phase 1: ids in slot order (sentinel in the padding), warp-local rows
+  int lq[R];  // cell of the row inside the warp (0..3)
+  bool real[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int jl = lane + 32 * r, j = j0 + jl;
+    real[r] = false;
+    lq[r] = 0;
+    if (j < j1) {
+      const int lc = T.cell[j];
+      lq[r] = lc - cw0;
+      real[r] = (uint32_t)j - T.off[lc] < T.cnt[lc];
+      W.id[jl] = real[r] ? T.p[j].id : kSentinel;
+    }
+  }
+  __syncwarp();
+
+  // phase 2: rank by id inside the cell, 4-wide over the padded segment;
+  // stage (m v, m) in rank order -- the reference permutation is the stable
+  // argsort over id order (collision.py:98)
+  int row[R];  // skewed staging row of the particle
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    row[r] = 0;
+    if (real[r]) {
+      const int jl = lane + 32 * r;
+      const int q = lq[r];
+      const int lo = (int)T.off[cw0 + q] - j0, hi = (int)T.off[cw0 + q + 1] - j0;
+      const uint32_t me = W.id[jl];
+      uint32_t rank = 0;
+#pragma unroll 1
+      for (int s = lo; s < hi; s += 4) {
+        const uint4 w = *reinterpret_cast<const uint4*>(W.id + s);
+        rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
+      }
+      row[r] = lo + (int)rank + q;
+      const VRec v = T.v[j0 + jl];
+      const double m = UMASS ? A.m0 : v.m;
+      double2* sv = reinterpret_cast<double2*>(W.val + row[r] * 4);
+      sv[0] = make_double2(m * v.vx, m * v.vy);
+      sv[1] = make_double2(m * v.vz, m);
+    }
+  }
+  __syncwarp();
+
+  // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206);
+  // four lanes per cell, com = p / m (collision.py:209-214) from the group's
+  // mass lane by shuffle
+  {
+    const int q = lane >> 2, comp = lane & 3;
+    const bool mine = lane < 4 * kCW && q < ncw;
+    double mom = 0.0;
+    if (mine) {
+      const int lc = cw0 + q;
+      mom = reduceat_col<4>(W.val + ((int)T.off[lc] - j0 + q) * 4 + comp, (int)T.cnt[lc]);
+    }
+    const double mass = __shfl_sync(0xffffffffu, mom, lane | 3);
+    if (mine) {
+      W.mom[lane] = mom;
+      const double c = (comp < 3) ? ((mass > 0.0) ? mom / mass : 0.0)
+                                  : (double)T.cnt[cw0 + q];
+      if (comp < 3) W.com[q * 3 + comp] = c;
+      else acc[4] += mass;
+      if (COM) A.com_cap[(c0 + cw0 + q) * 4 + comp] = c;
+    }
+  }
+  __syncwarp();
+
+  // phase 4: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
+  // next-step cell; claim every slot, then store; stage post-collision rows
+  double o[R][6];
+  uint32_t key[R];
+  double mm[R];
+  uint32_t pid[R];
+  bool stay[R];  // kMulti: the next cell is this domain's
+  int dest[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    key[r] = 0u;
+    stay[r] = real[r];
+    dest[r] = 0;
+    if (real[r]) {
+      const int j = j0 + lane + 32 * r;
+      const PRec p = T.p[j];
+      const VRec vr = T.v[j];
+      const double* cx = W.com + lq[r] * 3;
+      const double* ax = T.ax + (cw0 + lq[r]) * 3;
+      double v[3] = {vr.vx, vr.vy, vr.vz}, w[3];
+      rotate(v, cx, ax, A.cs, A.sn, w);
+      o[r][0] = wrap_fast(p.x + w[0] * A.dt, A.box0);
+      o[r][1] = wrap_fast(p.y + w[1] * A.dt, A.box1);
+      o[r][2] = wrap_fast(p.z + w[2] * A.dt, A.box2);
+      o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
+      pid[r] = p.id;
+      mm[r] = UMASS ? A.m0 : vr.m;
+      if (MODE == kMulti)
+        stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]);
+      else
+        key[r] = BYID ? p.id : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
+      const double m = mm[r];
+      double2* sv = reinterpret_cast<double2*>(W.val + row[r] * 4);
+      sv[0] = make_double2(m * w[0], m * w[1]);
+      sv[1] = make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]));
+    }
+  }
+  unsigned grp[R];
+  uint32_t base[R];
+  if (BYID) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (real[r])
+        store_rec(A.out, pid[r], o[r][0], o[r][1], o[r][2], pid[r], o[r][3], o[r][4], o[r][5],
+                  mm[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      grp[r] = 0u;
+      base[r] = 0u;
+      if (j0 + 32 * r < j1) {  // warp-uniform: every lane takes part in the ballot
+        if (MODE == kMulti)
+          send_foreign(A, real[r] && !stay[r], dest[r], o[r], pid[r], mm[r]);
+        claim_slot(A, stay[r], key[r], grp[r], base[r]);
+      }
+    }
+  }
+  __syncwarp();
+
+  // phase 5: conservation sums over the staged post rows, each lane its
+  // rank positions (fixed: deterministic) -- while the slot claims are in
+  // flight.  Position jl of cell q holds rank jl - lo_q, a real particle
+  // exactly when real[r].
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (real[r]) {
+      const int jl = lane + 32 * r;
+      const double2* sv = reinterpret_cast<const double2*>(W.val + (jl + lq[r]) * 4);
+      const double2 a = sv[0], c = sv[1];
+      acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
+    }
+  }
+  if (!BYID) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (stay[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
+  }
+  if (DRIFT) {
+    const int q = lane >> 2, comp = lane & 3;
+    double post = 0.0;
+    if (lane < 4 * kCW && q < ncw) {
+      const int lc = cw0 + q;
+      post = reduceat_col<4>(W.val + ((int)T.off[lc] - j0 + q) * 4 + comp, (int)T.cnt[lc]);
+    }
+    double* P = S.post + cw0 * 4;  // this pass's cells only
+    if (lane < 4 * ncw) P[lane] = post;
+    __syncwarp();
+    double worst = 0.0;
+    if (lane < ncw && W.mom[lane * 4 + 3] > 0.0)
+      worst = cell_drift(W.mom + lane * 4, P + lane * 4);
+    for (int off = 16; off > 0; off >>= 1)
+      worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+    if (lane == 0 && worst > 0.0) atomic_max_pos_double(A.drift_bits, worst);
+  }
+}
+
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
 __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int64_t ntiles) {
-  constexpr bool BYID = MODE == kById;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -488,13 +673,13 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   if (t == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.full[b], 2);
-      mbar_init(&S.empty[b], kNC / 32);
+      mbar_init(&S.empty[b], kNCW);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kNC / 32) {  // ------------------------------------ producer
+  if (warp == kNCW) {  // -------------------------------------- producer
     const uint64_t pol = policy_evict_first();
     int64_t tile = blockIdx.x;
     uint32_t cnt = tile_count(A, tile, ntiles);
@@ -508,187 +693,34 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     return;
   }
 
-  // ---------------------------------------------------------- consumers
+  // ------------------------------------------------------------ consumers
+  WarpScratch& W = S.w[warp];
+  const int cw0 = warp * kCW;  // this warp's first cell of every tile
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // px py pz sum(m v^2) mass
   int64_t tile = blockIdx.x;
   for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
     const int b = (int)(i & 1);
     TileBuf& T = S.buf[b];
     mbar_wait(&S.full[b], (uint32_t)(i >> 1) & 1u);
-    if (T.skip) {
-      consumer_sync();
+    const int64_t c0 = tile * kTC;
+    const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)kCW, A.C - c0 - cw0));
+    if (ncw == 0) {
+      __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[b]);
       continue;
     }
-    const int64_t c0 = tile * kTC;
-    const int nc = (int)min((int64_t)kTC, A.C - c0);
-    const int npad = (int)T.off[nc];
-
-    // phase 1: ids in slot order (sentinel in the padding); zero padding rows
-    int lcell[kPPTT];
-    bool real[kPPTT];
-#pragma unroll
-    for (int r = 0; r < kPPTT; ++r) {
-      const int j = r * kNC + t;
-      real[r] = false;
-      lcell[r] = 0;
-      if (j < npad) {
-        const int lc = T.cell[j];
-        lcell[r] = lc;
-        real[r] = (uint32_t)j - T.off[lc] < T.cnt[lc];
-        S.id[j] = real[r] ? T.p[j].id : kSentinel;
-        if (!real[r]) {
-          double2* sv = reinterpret_cast<double2*>(S.val + j * 4);
-          sv[0] = make_double2(0.0, 0.0);
-          sv[1] = make_double2(0.0, 0.0);
-        }
-      }
+    // The warp's cells in passes of at most kSlotsW padded slots: one pass
+    // almost always, two for the fullest quarter tiles (a cell never holds
+    // more than kSlotsW: the producer sends such tiles to k_step_dense).
+    for (int g0 = cw0, gend = cw0 + ncw; g0 < gend;) {
+      int g1 = g0 + 1;
+      while (g1 < gend && T.off[g1 + 1] - T.off[g0] <= (uint32_t)kSlotsW) ++g1;
+      consume_cells<kRowsW, UNIT, UMASS, DRIFT, COM, MODE>(A, S, T, W, c0, g0, g1 - g0,
+                                                           (int)T.off[g0], (int)T.off[g1], acc);
+      __syncwarp();  // W is rewritten by the next pass
+      g0 = g1;
     }
-    consumer_sync();
-
-    // phase 2: rank by id inside the cell, 4-wide over the padded segment;
-    // stage (m v, m) in rank order -- the reference permutation is the stable
-    // argsort over id order (collision.py:98)
-    int slot[kPPTT];
-#pragma unroll
-    for (int r = 0; r < kPPTT; ++r) {
-      slot[r] = 0;
-      if (real[r]) {
-        const int j = r * kNC + t;
-        const int lc = lcell[r];
-        const int lo = (int)T.off[lc], hi = (int)T.off[lc + 1];
-        const uint32_t me = S.id[j];
-        uint32_t rank = 0;
-#pragma unroll 1
-        for (int q = lo; q < hi; q += 4) {
-          const uint4 w = *reinterpret_cast<const uint4*>(S.id + q);
-          rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
-        }
-        slot[r] = lo + (int)rank;
-        const VRec v = T.v[j];
-        const double m = UMASS ? A.m0 : v.m;
-        double2* sv = reinterpret_cast<double2*>(S.val + slot[r] * 4);
-        sv[0] = make_double2(m * v.vx, m * v.vy);
-        sv[1] = make_double2(m * v.vz, m);
-      }
-    }
-    consumer_sync();
-
-    // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206)
-    // four lanes per cell; com = p / m (collision.py:209-214) from the
-    // group's mass lane by shuffle, so no barrier separates the two
-    static_assert(kNC >= 4 * kTC, "one moment task per consumer thread");
-    {
-      const int lc = t >> 2, comp = t & 3;
-      double mom = 0.0;
-      if (lc < nc) mom = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
-      const double mass = __shfl_sync(0xffffffffu, mom, lane | 3);
-      if (lc < nc) {
-        S.mom[t] = mom;
-        const double q = (comp < 3) ? ((mass > 0.0) ? mom / mass : 0.0) : (double)T.cnt[lc];
-        if (comp < 3) S.com[lc * 3 + comp] = q;
-        else acc[4] += mass;
-        if (COM) A.com_cap[(c0 + lc) * 4 + comp] = q;
-      }
-    }
-    consumer_sync();
-
-    // phase 5: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
-    // next-step cell; claim every slot, then store; stage post-collision rows
-    double o[kPPTT][6];
-    uint32_t key[kPPTT];
-    double mm[kPPTT];
-    uint32_t pid[kPPTT];
-    bool stay[kPPTT];  // kMulti: the next cell is this domain's
-    int dest[kPPTT];
-#pragma unroll
-    for (int r = 0; r < kPPTT; ++r) {
-      key[r] = 0u;
-      stay[r] = real[r];
-      dest[r] = 0;
-      if (real[r]) {
-        const int j = r * kNC + t;
-        const PRec p = T.p[j];
-        const VRec vr = T.v[j];
-        const double* cx = S.com + lcell[r] * 3;
-        const double* ax = T.ax + lcell[r] * 3;
-        double v[3] = {vr.vx, vr.vy, vr.vz}, w[3];
-        rotate(v, cx, ax, A.cs, A.sn, w);
-        o[r][0] = wrap_fast(p.x + w[0] * A.dt, A.box0);
-        o[r][1] = wrap_fast(p.y + w[1] * A.dt, A.box1);
-        o[r][2] = wrap_fast(p.z + w[2] * A.dt, A.box2);
-        o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
-        pid[r] = p.id;
-        mm[r] = UMASS ? A.m0 : vr.m;
-        if (MODE == kMulti)
-          stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]);
-        else
-          key[r] = BYID ? p.id : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
-        const double m = mm[r];
-        double2* sv = reinterpret_cast<double2*>(S.val + slot[r] * 4);
-        sv[0] = make_double2(m * w[0], m * w[1]);
-        sv[1] = make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]));
-      }
-    }
-    unsigned grp[kPPTT];
-    uint32_t base[kPPTT];
-    if (BYID) {
-#pragma unroll
-      for (int r = 0; r < kPPTT; ++r)
-        if (real[r])
-          store_rec(A.out, pid[r], o[r][0], o[r][1], o[r][2], pid[r], o[r][3], o[r][4], o[r][5],
-                    mm[r]);
-    } else {
-#pragma unroll
-      for (int r = 0; r < kPPTT; ++r) {
-        grp[r] = 0u;
-        base[r] = 0u;
-        if (r * kNC < npad) {  // warp-uniform: every lane takes part in the ballot
-          if (MODE == kMulti)
-            send_foreign(A, real[r] && !stay[r], dest[r], o[r], pid[r], mm[r]);
-          claim_slot(A, stay[r], key[r], grp[r], base[r]);
-        }
-      }
-    }
-    consumer_sync();
-    // the tile buffer is free for the producer (DRIFT still reads its
-    // off/cnt below and releases it after that)
-    if (!DRIFT && lane == 0) mbar_arrive(&S.empty[b]);
-
-    // phase 6: conservation sums over this thread's staged rows, in slot
-    // order (fixed: deterministic) -- while the slot claims are in flight
-#pragma unroll
-    for (int r = 0; r < kPPTT; ++r) {
-      const int j = r * kNC + t;
-      if (j < npad) {  // padding rows are zero
-        const double2* sv = reinterpret_cast<const double2*>(S.val + j * 4);
-        const double2 a = sv[0], c = sv[1];
-        acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
-      }
-    }
-    if (!BYID) {
-#pragma unroll
-      for (int r = 0; r < kPPTT; ++r)
-        if (stay[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
-    }
-    if (DRIFT) {
-      for (int task = t; task < nc * 4; task += kNC) {
-        const int lc = task >> 2, comp = task & 3;
-        S.post[task] = reduceat_col<4>(S.val + T.off[lc] * 4 + comp, (int)T.cnt[lc]);
-      }
-      consumer_sync();
-      if (lane == 0) mbar_arrive(&S.empty[b]);
-      if (warp == 1) {
-        double worst = 0.0;
-        for (int lc = lane; lc < nc; lc += 32)
-          if (S.mom[lc * 4 + 3] > 0.0)
-            worst = fmax(worst, cell_drift(S.mom + lc * 4, S.post + lc * 4));
-        for (int off = 16; off > 0; off >>= 1)
-          worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
-        if (lane == 0 && worst > 0.0) atomic_max_pos_double(A.drift_bits, worst);
-      }
-    }
-    consumer_sync();  // S.val / S.id are rewritten by the next tile
+    if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
   }
   // CTA partials: fixed-order block reduction of the per-thread sums
 #pragma unroll
@@ -700,7 +732,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   consumer_sync();
   if (t < 5) {
     double s = 0.0;
-    for (int w = 0; w < kNC / 32; ++w) s += S.red[w * 5 + t];
+    for (int w = 0; w < kNCW; ++w) s += S.red[w * 5 + t];
     A.partials[(int64_t)blockIdx.x * 8 + t] = s;
   }
 }
