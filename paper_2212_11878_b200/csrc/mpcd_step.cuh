@@ -192,6 +192,21 @@ __device__ __forceinline__ double wrap_fast(double x, double box) {
 // numpy pairwise leaf, compile-time stride, 32-bit indices
 template <int S>
 __device__ __forceinline__ double pw_leaf(const double* t, int n) {
+  if (n < 16) {  // the common cell sizes, predicated instead of looped (same association)
+    if (n < 8) {
+      double res = 0.0;
+#pragma unroll
+      for (int i = 0; i < 7; ++i)
+        if (i < n) res += t[i * S];
+      return res;
+    }
+    double res = ((t[0] + t[S]) + (t[2 * S] + t[3 * S])) +
+                 ((t[4 * S] + t[5 * S]) + (t[6 * S] + t[7 * S]));
+#pragma unroll
+    for (int i = 8; i < 15; ++i)
+      if (i < n) res += t[i * S];
+    return res;
+  }
   if (n < 8) {
     double res = 0.0;
     for (int i = 0; i < n; ++i) res += t[i * S];
@@ -237,11 +252,21 @@ __device__ __forceinline__ double cell_drift(const double* pre, const double* po
 // Slot claims in the next binning, batched so that every atomic of a thread
 // is in flight before any result is used.  One atomic per distinct
 // destination cell per warp (match_any aggregation).
+// Slot claims: one atomic per particle (MPCD_NOAGG=1, measured faster on
+// B200 than warp aggregation with match_any: the atomics' L2 throughput is
+// ample and the aggregation's MATCH / shuffle latency sat on the critical path)
+#ifndef MPCD_NOAGG
+#define MPCD_NOAGG 1
+#endif
 __device__ __forceinline__ void claim_slot(const StepArgs& A, bool active, uint32_t key,
                                            unsigned& grp, uint32_t& base) {
-  const unsigned act = __ballot_sync(0xffffffffu, active);
   grp = 0u;
   base = 0u;
+  if (MPCD_NOAGG) {  // one atomic per particle: the slot itself
+    if (active) base = atomicAdd(&A.count_out[key], 1u);
+    return;
+  }
+  const unsigned act = __ballot_sync(0xffffffffu, active);
   if (active) {
     grp = __match_any_sync(act, key);
     if ((int)(threadIdx.x & 31) == __ffs(grp) - 1)
@@ -254,8 +279,11 @@ __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, uns
                                             uint32_t base, const double* o, uint32_t id,
                                             double m) {
   const int lane = threadIdx.x & 31;
-  base = __shfl_sync(grp, base, __ffs(grp) - 1);
-  const uint32_t slot = base + (uint32_t)__popc(grp & ((1u << lane) - 1u));
+  uint32_t slot = base;
+  if (!MPCD_NOAGG) {
+    base = __shfl_sync(grp, base, __ffs(grp) - 1);
+    slot = base + (uint32_t)__popc(grp & ((1u << lane) - 1u));
+  }
   if (slot < A.cap) {
     store_rec(A.out, (uint64_t)key * A.cap + slot, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
   } else {  // full cell: overflow list (gathered by the dense kernel next step)
@@ -712,9 +740,14 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     // The warp's cells in passes of at most kSlotsW padded slots: one pass
     // almost always, two for the fullest quarter tiles (a cell never holds
     // more than kSlotsW: the producer sends such tiles to k_step_dense).
-    for (int g0 = cw0, gend = cw0 + ncw; g0 < gend;) {
-      int g1 = g0 + 1;
-      while (g1 < gend && T.off[g1 + 1] - T.off[g0] <= (uint32_t)kSlotsW) ++g1;
+    const int gend = cw0 + ncw;
+    const bool one = T.off[gend] - T.off[cw0] <= (uint32_t)kSlotsW;
+    for (int g0 = cw0; g0 < gend;) {
+      int g1 = gend;
+      if (!one) {
+        g1 = g0 + 1;
+        while (g1 < gend && T.off[g1 + 1] - T.off[g0] <= (uint32_t)kSlotsW) ++g1;
+      }
       consume_cells<kRowsW, UNIT, UMASS, DRIFT, COM, MODE>(A, S, T, W, c0, g0, g1 - g0,
                                                            (int)T.off[g0], (int)T.off[g1], acc);
       __syncwarp();  // W is rewritten by the next pass
