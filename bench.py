@@ -35,17 +35,20 @@ METRIC = "MPCD particle-steps/sec"
 UNIT = "particle-steps/s"
 PPC = 10.0
 
-# Algorithmic bytes of one launch, per particle (n) and per cell (C)
-# (DESIGN.md section 3).  A particle is two 32-byte records; k_step reads
-# each once from its cell region and writes it once into its next-step cell;
-# per cell it reads + zeroes this step's count, updates the next count
-# (atomic, 8) and writes 64 B of partials per 32-cell tile.
+# Roofline numerator: SURVEY.md 8(d)'s per-unit
+# algorithmic bytes of the MPCD step, B_alg = 216 B per particle + 28 B per
+# cell -- the compulsory traffic of the sort-based step the survey models --
+# times the particles and cells one k_step launch processes.  Reported beside
+# it: this design's own bytes (a particle is two 32-byte records, read once
+# from its cell region and written once into its next-step cell: 128 B; per
+# cell read + zero its count and one atomic on the next count: 16 B) and the
+# compulsory floor B_min (read + write x, v once: 96 B).
 KERNELS = ("k_step", "k_step_dense", "k_diag")  # mpcd_read_profile slots 0..2
 # k_step, k_sort_dense, k_step_dense, k_diag_partial, k_diag_finalize
 # (+ k_place_xrecs, the absorb of received particles, in a decomposed box)
 LAUNCHES_PER_STEP = 5
-BYTES_PER_N = {"k_step": 128, "k_step_dense": 0, "k_diag": 0}
-BYTES_PER_C = {"k_step": 16 + 64.0 / 32, "k_step_dense": 0, "k_diag": 64.0 / 32}
+BYTES_PER_N = {"k_step": 128, "k_step_dense": 0, "k_diag": 0}   # this design
+BYTES_PER_C = {"k_step": 16, "k_step_dense": 0, "k_diag": 0}
 SURVEY_B_ALG_N, SURVEY_B_ALG_C = 216, 28  # B_alg = 216 n + 28 C
 B_MIN_N = 96                              # compulsory: read + write x, v once
 
@@ -281,9 +284,11 @@ def run_ours(args):
     lib.mpcd_profile(ctx.handle, 0)
     per_kernel = {k: kms[i] / max(nst.value, 1) for i, k in enumerate(KERNELS)}
     top = max(per_kernel, key=per_kernel.get)
-    alg = {k: BYTES_PER_N[k] * n + BYTES_PER_C[k] * C for k in KERNELS}
+    alg = {k: BYTES_PER_N[k] * n + BYTES_PER_C[k] * C for k in KERNELS}  # design bytes
     peak, peak_src = peaks()
-    achieved = alg[top] / (per_kernel[top] * 1e-3) / 1e9
+    survey_launch = SURVEY_B_ALG_N * n + SURVEY_B_ALG_C * C  # k_step does the whole step
+    achieved = survey_launch / (per_kernel[top] * 1e-3) / 1e9
+    design_achieved = alg[top] / (per_kernel[top] * 1e-3) / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -312,7 +317,13 @@ def run_ours(args):
                    "l2": "state 17 GB >> 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": alg[top],
+                     "algorithmic_bytes_per_launch": survey_launch,
+                     "bytes_model": "SURVEY.md 8(d): 216 B/particle + 28 B/cell",
+                     "design_bytes_per_launch": alg[top],
+                     "design_achieved": design_achieved, "design_frac": design_achieved / peak,
+                     "b_min_frac": B_MIN_N * n / (per_kernel[top] * 1e-3) / 1e9 / peak,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "
+                                       "dram__bytes_read.sum + dram__bytes_write.sum)",
                      "avg_launch_ms": per_kernel[top], "peak_source": peak_src},
         "roofline_step": {
             "bytes_per_step": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9,

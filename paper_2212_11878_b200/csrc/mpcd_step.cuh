@@ -431,13 +431,18 @@ struct __align__(16) WarpScratch {
   double com[kCW * 3];
 };
 
+#ifndef MPCD_STAGES
+#define MPCD_STAGES 2
+#endif
+constexpr int kStages = MPCD_STAGES;  // tile buffers in flight per CTA
+
 template <bool DRIFT>
 struct StepSmem {
-  TileBuf buf[2];
+  TileBuf buf[kStages];
   WarpScratch w[kNCW];
   double post[DRIFT ? kTC * 4 : 1];
   double red[kNCW * 5];
-  uint64_t full[2], empty[2];
+  uint64_t full[kStages], empty[kStages];
 };
 
 __device__ __forceinline__ void consumer_sync() {
@@ -699,7 +704,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t G = gridDim.x;
   if (t == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kStages; ++b) {
       mbar_init(&S.full[b], 2);
       mbar_init(&S.empty[b], kNCW);
     }
@@ -712,9 +717,9 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     int64_t tile = blockIdx.x;
     uint32_t cnt = tile_count(A, tile, ntiles);
     for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
-      const int b = (int)(i & 1);
+      const int b = (int)(i % kStages);
       const uint32_t cnt_next = tile_count(A, tile + G, ntiles);  // in flight meanwhile
-      if (i >= 2) mbar_wait(&S.empty[b], (uint32_t)((i >> 1) - 1) & 1u);
+      if (i >= kStages) mbar_wait(&S.empty[b], (uint32_t)((i / kStages) - 1) & 1u);
       prepare_tile<MODE>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
       cnt = cnt_next;
     }
@@ -727,9 +732,9 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // px py pz sum(m v^2) mass
   int64_t tile = blockIdx.x;
   for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
-    const int b = (int)(i & 1);
+    const int b = (int)(i % kStages);
     TileBuf& T = S.buf[b];
-    mbar_wait(&S.full[b], (uint32_t)(i >> 1) & 1u);
+    mbar_wait(&S.full[b], (uint32_t)(i / kStages) & 1u);
     const int64_t c0 = tile * kTC;
     const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)kCW, A.C - c0 - cw0));
     if (ncw == 0) {
