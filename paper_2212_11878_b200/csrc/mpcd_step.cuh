@@ -344,6 +344,21 @@ __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, 
   if (local) finish_slot(A, key, grp, base, o, id, m);
 }
 
+// ----------------------------------------------- shared-memory row access --
+// The two 16-byte halves of a 32-byte row.  (Swizzling the half order by
+// row to avoid the 2-way bank conflict of the 32-byte stride was measured
+// slower on B200: the selects cost more issue slots than the conflicts.)
+__device__ __forceinline__ void lds_row32(const void* base, int row, double2& lo, double2& hi) {
+  const double2* p = reinterpret_cast<const double2*>(base) + 2 * row;
+  lo = p[0];
+  hi = p[1];
+}
+__device__ __forceinline__ void sts_row32(void* base, int row, double2 lo, double2 hi) {
+  double2* p = reinterpret_cast<double2*>(base) + 2 * row;
+  p[0] = lo;
+  p[1] = hi;
+}
+
 // ------------------------------------------------------------ TMA helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -569,11 +584,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
         rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
       }
       row[r] = lo + (int)rank + q;
-      const VRec v = T.v[j0 + jl];
-      const double m = UMASS ? A.m0 : v.m;
-      double2* sv = reinterpret_cast<double2*>(W.val + row[r] * 4);
-      sv[0] = make_double2(m * v.vx, m * v.vy);
-      sv[1] = make_double2(m * v.vz, m);
+      double2 v01, v23;  // vx vy | vz m
+      lds_row32(T.v, j0 + jl, v01, v23);
+      const double m = UMASS ? A.m0 : v23.y;
+      sts_row32(W.val, row[r], make_double2(m * v01.x, m * v01.y), make_double2(m * v23.x, m));
     }
   }
   __syncwarp();
@@ -616,26 +630,26 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     dest[r] = 0;
     if (real[r]) {
       const int j = j0 + lane + 32 * r;
-      const PRec p = T.p[j];
-      const VRec vr = T.v[j];
+      double2 p01, p23, v01, v23;  // x y | z id, vx vy | vz m
+      lds_row32(T.p, j, p01, p23);
+      lds_row32(T.v, j, v01, v23);
       const double* cx = W.com + lq[r] * 3;
       const double* ax = T.ax + (cw0 + lq[r]) * 3;
-      double v[3] = {vr.vx, vr.vy, vr.vz}, w[3];
+      double v[3] = {v01.x, v01.y, v23.x}, w[3];
       rotate(v, cx, ax, A.cs, A.sn, w);
-      o[r][0] = wrap_fast(p.x + w[0] * A.dt, A.box0);
-      o[r][1] = wrap_fast(p.y + w[1] * A.dt, A.box1);
-      o[r][2] = wrap_fast(p.z + w[2] * A.dt, A.box2);
+      o[r][0] = wrap_fast(p01.x + w[0] * A.dt, A.box0);
+      o[r][1] = wrap_fast(p01.y + w[1] * A.dt, A.box1);
+      o[r][2] = wrap_fast(p23.x + w[2] * A.dt, A.box2);
       o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
-      pid[r] = p.id;
-      mm[r] = UMASS ? A.m0 : vr.m;
+      pid[r] = bits_id(p23.y);
+      mm[r] = UMASS ? A.m0 : v23.y;
       if (MODE == kMulti)
         stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]);
       else
-        key[r] = BYID ? p.id : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
+        key[r] = BYID ? pid[r] : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
       const double m = mm[r];
-      double2* sv = reinterpret_cast<double2*>(W.val + row[r] * 4);
-      sv[0] = make_double2(m * w[0], m * w[1]);
-      sv[1] = make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]));
+      sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]),
+                make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2])));
     }
   }
   unsigned grp[R];
@@ -668,8 +682,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   for (int r = 0; r < R; ++r) {
     if (real[r]) {
       const int jl = lane + 32 * r;
-      const double2* sv = reinterpret_cast<const double2*>(W.val + (jl + lq[r]) * 4);
-      const double2 a = sv[0], c = sv[1];
+      double2 a, c;
+      lds_row32(W.val, jl + lq[r], a, c);
       acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
     }
   }
