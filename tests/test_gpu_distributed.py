@@ -43,6 +43,8 @@ def run(params, backend, n_steps, **kw):
     ((16, 16, 16), (1, 2, 2)),
     ((16, 16, 16), (2, 2, 2)),
     ((24, 16, 8), (4, 2, 1)),   # non-cubic, pencil (the config-5 shape in small)
+    ((8, 8, 8), (8, 1, 1)),     # one-cell slabs: most particles change owner every step
+    ((4, 4, 4), (2, 2, 4)),     # 1-2 cells per domain axis, 16 domains
 ])
 def test_sequential_domains_bitwise_equal_whole_box(dims, rank_dims):
     base = mp.SimParams(edge_length=dims[0], edge_lengths=dims, seed=11)

@@ -1,10 +1,12 @@
-# One gpurun call: GPU tests, bench (N=1), a 2-rank functional check of the
-# decomposed bench path on one GPU (gloo), launch list, one ncu capture.
+# One gpurun call: GPU tests, smoke, bench (N=1), a 2-rank functional check
+# of the decomposed bench path on one GPU (gloo), launch list, one ncu capture.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; tail -2 gpurun_out/bench.log
+timeout 300 python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1; tail -1 gpurun_out/bench_reference.log
 MPCD_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
   --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --L 64 --steps 5 --warmup 3 \
   > gpurun_out/bench_2rank_gloo.log 2>&1; tail -2 gpurun_out/bench_2rank_gloo.log
