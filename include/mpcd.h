@@ -84,8 +84,9 @@ typedef struct {
   double energy;
   double mass;
   double max_cell_drift; /* valid when the step had MPCD_STEP_WANT_DRIFT */
-  int64_t n;
+  int64_t n;             /* particles this context collided in the step */
   int64_t step;          /* index of the step these describe */
+  int64_t migrated;      /* of them, particles that moved to another domain */
 } mpcd_diag;
 
 typedef struct mpcd_ctx mpcd_ctx;
@@ -199,6 +200,24 @@ int mpcd_exchange_buffers(mpcd_ctx* ctx, mpcd_exchange* out);
 /* Bin n_recv received DEVICE records for the next step, account for the
  * n_sent this domain gave away, and clear send_n. */
 int mpcd_absorb(mpcd_ctx* ctx, const void* recs, int64_t n_recv, int64_t n_sent, void* stream);
+
+/* Fused migration (the B200 path): instead of send buffers, k_step writes a
+ * leaving particle straight into its new owner's next-step cell region --
+ * slot claimed by an atomic on the owner's count, record stored -- over peer
+ * memory (NVLink P2P stores and atomics between GPUs of a node).  After
+ * connecting, mpcd_step alone advances the domain; no mpcd_absorb.  The
+ * caller fences every step across ranks (e.g. a one-element NCCL all-reduce
+ * enqueued on the stream after mpcd_step): all ranks' step k must complete
+ * before any rank's step k+1 reads its cells.
+ *
+ * mpcd_ipc_handles exports this context's region / count / overflow
+ * allocations as CUDA IPC handles (*nbytes bytes; out = NULL asks the size);
+ * mpcd_connect_peers takes every rank's handles concatenated in rank order
+ * and opens the others'.  Domains of one process (one GPU or several)
+ * connect directly with mpcd_connect_local(ctxs[rank], n). */
+int mpcd_ipc_handles(mpcd_ctx* ctx, void* out, int64_t* nbytes);
+int mpcd_connect_peers(mpcd_ctx* ctx, const void* all_handles, int32_t n_ranks);
+int mpcd_connect_local(mpcd_ctx* const* ctxs, int32_t n);
 
 /* ------------------------------------------------------ host RNG helpers */
 uint64_t mpcd_key_state(uint64_t seed, uint64_t step, uint64_t purpose, uint64_t cell);

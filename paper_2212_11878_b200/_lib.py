@@ -50,6 +50,7 @@ class MpcdDiag(C.Structure):
         ("max_cell_drift", C.c_double),
         ("n", C.c_int64),
         ("step", C.c_int64),
+        ("migrated", C.c_int64),
     ]
 
 
@@ -93,6 +94,9 @@ SIGNATURES = {
     "mpcd_ctx_set_domain": (C.c_int, [_vp, C.POINTER(MpcdDomain)]),
     "mpcd_exchange_buffers": (C.c_int, [_vp, C.POINTER(MpcdExchange)]),
     "mpcd_absorb": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp]),
+    "mpcd_ipc_handles": (C.c_int, [_vp, _vp, _i64]),
+    "mpcd_connect_peers": (C.c_int, [_vp, _vp, C.c_int32]),
+    "mpcd_connect_local": (C.c_int, [C.POINTER(_vp), C.c_int32]),
     "mpcd_profile": (C.c_int, [_vp, C.c_int32]),
     "mpcd_read_profile": (C.c_int, [_vp, _d, _i64]),
     "mpcd_key_state": (C.c_uint64, [C.c_uint64] * 4),

@@ -150,6 +150,19 @@ __global__ void k_place_flat(Recs flat, int64_t n, PlaceArgs P) {
   }
 }
 
+// particles resident in region set b: sum of min(count, cap) + overflow entries
+__global__ void k_count_resident(const uint32_t* count, int64_t C, uint32_t cap,
+                                 const uint32_t* ovf_n, uint32_t ovf_cap,
+                                 unsigned long long* out) {
+  unsigned long long s = 0;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
+       c += (int64_t)gridDim.x * blockDim.x)
+    s += min(count[c], cap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s += min(*ovf_n, ovf_cap);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
 __global__ void k_clamp_counts(const uint32_t* count, int64_t C, uint32_t cap, uint32_t* out) {
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
        c += (int64_t)gridDim.x * blockDim.x)
@@ -367,6 +380,11 @@ struct mpcd_ctx {
   int64_t org[3] = {0, 0, 0};
   XRec* send = nullptr;
   unsigned long long* send_n = nullptr;
+  // fused migration (mpcd_connect_peers / mpcd_connect_local)
+  bool p2p = false;
+  bool n_stale = false;      // c->n unknown on the host since the last fused step
+  PeerBufs* d_peers = nullptr;
+  std::vector<void*> ipc_opened;
 };
 
 namespace {
@@ -452,6 +470,24 @@ T* mapped(T* p) {
   if (a.type == cudaMemoryTypeHost && a.devicePointer) return static_cast<T*>(a.devicePointer);
   if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return p;
   return nullptr;
+}
+
+// Refresh c->n after fused steps (peers added and removed particles).
+int refresh_n(mpcd_ctx* c, cudaStream_t st) {
+  if (!c->n_stale) return MPCD_OK;
+  unsigned long long* d = nullptr;
+  unsigned long long h = 0;
+  MPCD_CUDA(cudaMallocAsync(&d, sizeof(*d), st));
+  MPCD_CUDA(cudaMemsetAsync(d, 0, sizeof(*d), st));
+  k_count_resident<<<grid_for(c->C, 256), 256, 0, st>>>(c->count[c->cur], c->C, c->cap,
+                                                       ovf_n_of(c, c->cur), c->ovf_cap, d);
+  MPCD_LAUNCH_CHECK();
+  MPCD_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  MPCD_CUDA(cudaFreeAsync(d, st));
+  MPCD_CUDA(cudaStreamSynchronize(st));
+  c->n = (int64_t)h;
+  c->n_stale = false;
+  return MPCD_OK;
 }
 
 // particles placed by the last filtered placement (multi-domain upload/init)
@@ -579,6 +615,8 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.m0 = g.mass_value;
   A.part_base = 0;
   (void)by_id;
+  A.peers = c->p2p ? c->d_peers : nullptr;
+  A.out_set = b ^ 1;
   if (c->multi) {
     A.G0 = (int)c->dom.global_dims[0]; A.G1 = (int)c->dom.global_dims[1];
     A.G2 = (int)c->dom.global_dims[2];
@@ -699,7 +737,7 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
   if (ev) MPCD_CUDA(cudaEventRecord(ev[2], st));
   k_diag_partial<<<kDiagBlocks, 256, 0, st>>>(c->partials, nparts, c->level1);
   MPCD_LAUNCH_CHECK();
-  k_diag_finalize<<<1, 32, 0, st>>>(c->level1, kDiagBlocks, c->drift_bits, c->diag, c->n, step,
+  k_diag_finalize<<<1, 32, 0, st>>>(c->level1, kDiagBlocks, c->drift_bits, c->diag, step,
                                     flags_of(c), ovf_n_of(c, c->cur), scratch_n_of(c));
   MPCD_LAUNCH_CHECK();
   if (ev) MPCD_CUDA(cudaEventRecord(ev[3], st));
@@ -714,12 +752,17 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
   c->have_diag = true;
   c->last_com = com;
   c->last_step = step;
+  if (c->p2p) c->n_stale = true;  // particles arrived from / left to peers
   return MPCD_OK;
 }
 
 int download_rows(mpcd_ctx* c, double* pos, double* vel, double* mass, int64_t* ids,
                   int32_t id_order, void* stream) {
   cudaStream_t st = as_stream(stream);
+  {
+    int rc = refresh_n(c, st);
+    if (rc) return rc;
+  }
   const int64_t n = c->n;
   if (n == 0) return MPCD_OK;
   Recs rows;
@@ -777,6 +820,8 @@ int download_rows(mpcd_ctx* c, double* pos, double* vel, double* mass, int64_t* 
 // the host when id_order is asked for.
 int download_multi(mpcd_ctx* c, double* pos, double* vel, double* mass, int64_t* ids,
                    int32_t id_order, void* stream) {
+  int rc0 = refresh_n(c, as_stream(stream));
+  if (rc0) return rc0;
   const int64_t n = c->n;
   std::vector<double> hp(3 * n), hv(3 * n), hm(n);
   std::vector<int64_t> hi(n);
@@ -857,12 +902,12 @@ int mpcd_ctx_create(const mpcd_config* cfg, mpcd_ctx** out) {
       cudaMalloc(&c->scratch_src, sizeof(uint32_t) * c->scratch_cap) != cudaSuccess ||
       cudaMalloc(&c->scratch_val, sizeof(double) * 4 * c->scratch_cap) != cudaSuccess ||
       cudaMalloc(&c->partials, sizeof(double) * 8 * (c->ntiles + kDenseGrid)) != cudaSuccess ||
-      cudaMalloc(&c->level1, sizeof(double) * 5 * kDiagBlocks) != cudaSuccess ||
-      cudaMalloc(&c->diag, sizeof(double) * 8) != cudaSuccess ||
+      cudaMalloc(&c->level1, sizeof(double) * kDiagCols * kDiagBlocks) != cudaSuccess ||
+      cudaMalloc(&c->diag, sizeof(double) * 16) != cudaSuccess ||
       cudaMalloc(&c->drift_bits, sizeof(unsigned long long)) != cudaSuccess)
     return cleanup(fail(MPCD_ERR_CUDA, "cudaMalloc of per-tile arrays failed"));
   cudaMemset(c->small, 0, sizeof(uint32_t) * 8);
-  cudaMemset(c->diag, 0, sizeof(double) * 8);
+  cudaMemset(c->diag, 0, sizeof(double) * 16);
   cudaMemset(c->drift_bits, 0, sizeof(unsigned long long));
   int rc = c->scan.init(C);
   if (rc) return cleanup(rc);
@@ -889,12 +934,21 @@ int mpcd_ctx_destroy(mpcd_ctx* c) {
   for (cudaEvent_t e : c->prof_events) cudaEventDestroy(e);
   if (c->send) cudaFree(c->send);
   if (c->send_n) cudaFree(c->send_n);
+  if (c->d_peers) cudaFree(c->d_peers);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   c->scan.release();
   delete c;
   return MPCD_OK;
 }
 
-int64_t mpcd_count(const mpcd_ctx* c) { return c ? c->n : -1; }
+int64_t mpcd_count(const mpcd_ctx* c) {
+  if (!c) return -1;
+  if (c->n_stale) {  // after fused steps: count on the device (synchronises the null stream)
+    DeviceGuard dg(c->dev);
+    if (refresh_n(const_cast<mpcd_ctx*>(c), nullptr)) return -1;
+  }
+  return c->n;
+}
 int64_t mpcd_current_step(const mpcd_ctx* c) { return c ? c->cur_step : -1; }
 int64_t mpcd_cell_capacity(const mpcd_ctx* c) { return c ? (int64_t)c->cap : -1; }
 
@@ -997,7 +1051,7 @@ int mpcd_read_diag(mpcd_ctx* c, mpcd_diag* out, void* stream) {
   if (!c || !out) return fail(MPCD_ERR_CONFIG, "null argument");
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
-  double h[8];
+  double h[9];
   MPCD_CUDA(cudaMemcpyAsync(h, c->diag, sizeof(h), cudaMemcpyDeviceToHost, st));
   int rc = check_flags(c, st);  // synchronises
   if (rc) return rc;
@@ -1007,6 +1061,7 @@ int mpcd_read_diag(mpcd_ctx* c, mpcd_diag* out, void* stream) {
   out->max_cell_drift = h[5];
   out->n = (int64_t)h[6];
   out->step = c->have_diag ? (int64_t)h[7] : -1;
+  out->migrated = (int64_t)h[8];
   return MPCD_OK;
 }
 
@@ -1236,6 +1291,104 @@ int mpcd_absorb(mpcd_ctx* c, const void* recs, int64_t n_recv, int64_t n_sent, v
   const int64_t P = c->dom.rank_dims[0] * c->dom.rank_dims[1] * c->dom.rank_dims[2];
   MPCD_CUDA(cudaMemsetAsync(c->send_n, 0, sizeof(unsigned long long) * P, st));
   c->n += n_recv - n_sent;
+  return MPCD_OK;
+}
+
+// ---------------------------------------------------- fused migration ---
+namespace {
+constexpr int kIpcAllocs = 9;  // slab[2], count[2], ovf_slab[2], ovf_cell[2], small
+
+PeerBufs local_bufs(mpcd_ctx* c) {
+  PeerBufs P;
+  for (int b = 0; b < 2; ++b) {
+    P.reg[b] = c->reg[b];
+    P.count[b] = c->count[b];
+    P.ovf[b] = c->ovf[b];
+    P.ovf_cell[b] = c->ovf_cell[b];
+  }
+  P.small = c->small;
+  return P;
+}
+
+int install_peers(mpcd_ctx* c, const std::vector<PeerBufs>& tab) {
+  const int64_t P = (int64_t)c->dom.rank_dims[0] * c->dom.rank_dims[1] * c->dom.rank_dims[2];
+  if ((int64_t)tab.size() != P) return fail(MPCD_ERR_TOPOLOGY, "peer table has %d of %lld ranks",
+                                            (int)tab.size(), (long long)P);
+  if (c->d_peers) cudaFree(c->d_peers);
+  MPCD_CUDA(cudaMalloc(&c->d_peers, sizeof(PeerBufs) * P));
+  MPCD_CUDA(cudaMemcpy(c->d_peers, tab.data(), sizeof(PeerBufs) * P, cudaMemcpyHostToDevice));
+  c->p2p = true;
+  return MPCD_OK;
+}
+}  // namespace
+
+int mpcd_ipc_handles(mpcd_ctx* c, void* out, int64_t* nbytes) {
+  clear_error();
+  if (!c || !nbytes) return fail(MPCD_ERR_CONFIG, "null argument");
+  const int64_t need = kIpcAllocs * (int64_t)sizeof(cudaIpcMemHandle_t);
+  if (!out) {
+    *nbytes = need;
+    return MPCD_OK;
+  }
+  if (*nbytes < need) return fail(MPCD_ERR_CONFIG, "handle buffer needs %lld bytes", (long long)need);
+  DeviceGuard dg(c->dev);
+  void* allocs[kIpcAllocs] = {c->slab[0], c->slab[1], c->count[0], c->count[1], c->ovf_slab[0],
+                              c->ovf_slab[1], c->ovf_cell[0], c->ovf_cell[1], c->small};
+  cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(out);
+  for (int i = 0; i < kIpcAllocs; ++i) MPCD_CUDA(cudaIpcGetMemHandle(&h[i], allocs[i]));
+  *nbytes = need;
+  return MPCD_OK;
+}
+
+int mpcd_connect_peers(mpcd_ctx* c, const void* all, int32_t n_ranks) {
+  clear_error();
+  if (!c || !all) return fail(MPCD_ERR_CONFIG, "null argument");
+  if (!c->multi) return fail(MPCD_ERR_CONFIG, "not a decomposed domain (mpcd_ctx_set_domain)");
+  DeviceGuard dg(c->dev);
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all);
+  const uint64_t rows = (uint64_t)c->C * c->cap, orows = c->ovf_cap;
+  std::vector<PeerBufs> tab(n_ranks);
+  for (int r = 0; r < n_ranks; ++r) {
+    if (r == c->dom.rank) {
+      tab[r] = local_bufs(c);
+      continue;
+    }
+    void* p[kIpcAllocs];
+    for (int i = 0; i < kIpcAllocs; ++i) {
+      MPCD_CUDA(cudaIpcOpenMemHandle(&p[i], h[r * kIpcAllocs + i],
+                                     cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(p[i]);
+    }
+    // every rank has the same cells per domain, cap and overflow capacity
+    PeerBufs& P = tab[r];
+    for (int b = 0; b < 2; ++b) {
+      P.reg[b] = carve(p[b], rows);
+      P.count[b] = static_cast<uint32_t*>(p[2 + b]);
+      P.ovf[b] = carve(p[4 + b], orows);
+      P.ovf_cell[b] = static_cast<uint32_t*>(p[6 + b]);
+    }
+    P.small = static_cast<uint32_t*>(p[8]);
+  }
+  return install_peers(c, tab);
+}
+
+int mpcd_connect_local(mpcd_ctx* const* ctxs, int32_t n) {
+  clear_error();
+  if (!ctxs || n < 1) return fail(MPCD_ERR_CONFIG, "null argument");
+  std::vector<PeerBufs> tab(n);
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r] || !ctxs[r]->multi || ctxs[r]->dom.rank != r)
+      return fail(MPCD_ERR_TOPOLOGY, "context %d is not domain %d of the box", r, r);
+    if (ctxs[r]->C != ctxs[0]->C || ctxs[r]->cap != ctxs[0]->cap ||
+        ctxs[r]->ovf_cap != ctxs[0]->ovf_cap || ctxs[r]->dev != ctxs[0]->dev)
+      return fail(MPCD_ERR_TOPOLOGY, "domains differ in cells, capacities or device");
+    tab[r] = local_bufs(ctxs[r]);
+  }
+  for (int r = 0; r < n; ++r) {
+    DeviceGuard dg(ctxs[r]->dev);
+    int rc = install_peers(ctxs[r], tab);
+    if (rc) return rc;
+  }
   return MPCD_OK;
 }
 

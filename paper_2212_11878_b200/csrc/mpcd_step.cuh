@@ -64,6 +64,19 @@ __device__ __forceinline__ void store_rec(const Recs& s, uint64_t dst, double x,
   st2(&vr->vz, vz, m);
 }
 
+// The next-step buffers of every rank of a decomposed box, as this device
+// addresses them (its own, or peer memory opened from another process's CUDA
+// IPC handles, or another context of this process): the fused migration of
+// k_step writes a leaving particle straight into its new owner's cell region.
+// Index [b] = region set b (all ranks flip in lockstep).
+struct PeerBufs {
+  Recs reg[2];
+  uint32_t* count[2];
+  Recs ovf[2];
+  uint32_t* ovf_cell[2];
+  uint32_t* small;  // [2] overflow-list-full flag, [4 + b] overflow entries of set b
+};
+
 struct StepArgs {
   Recs in, out;               // regions of this step / of the next step
   uint32_t* count_in;         // per cell of this step (zeroed once consumed)
@@ -102,6 +115,8 @@ struct StepArgs {
   XRec* send;
   unsigned long long* send_n;  // claimed per destination (may exceed send_cap)
   uint32_t send_cap;
+  const PeerBufs* peers;       // non-null: fused migration over peer memory
+  int out_set;                 // region set the step writes (the same on every rank)
 };
 
 // Step kernel modes: binned single domain, by-id pure function, multi-domain
@@ -132,6 +147,7 @@ constexpr int kNT = 256;        // threads of the step CTA
 constexpr int kPPT = 3;         // staged particles per thread
 constexpr int kMaxP = kNT * kPPT;  // padded staging slots per tile
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+constexpr int kDiagCols = 7;  // partial columns: px py pz sum(m v^2) mass collided migrated
 
 // ------------------------------------------------------------ cell index --
 __device__ __noinline__ int cell_coord_slow(double t, int L) {
@@ -172,7 +188,9 @@ __device__ __forceinline__ bool next_cell_multi(const StepArgs& A, double x, dou
     return true;
   }
   dest = ((gx / A.L0) * A.R1 + gy / A.L1) * A.R2 + gz / A.L2;
-  key = 0u;
+  // the cell in the owner's numbering (uniform blocks: global mod block)
+  key = ((unsigned)(gx % A.L0) * (unsigned)A.L1 + (unsigned)(gy % A.L1)) * (unsigned)A.L2 +
+        (unsigned)(gz % A.L2);
   return false;
 }
 
@@ -301,9 +319,30 @@ __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, uns
 // destination's count may run past send_cap (the host sees it and fails).
 // Must be reached by the whole warp.
 __device__ __forceinline__ void send_foreign(const StepArgs& A, bool active, int dest,
-                                             const double* o, uint32_t id, double m) {
+                                             uint32_t key, const double* o, uint32_t id,
+                                             double m, double& migrated) {
+  if (A.peers) {  // fused: claim a slot in the owner's next-step cell, store there
+    if (!active) return;
+    migrated += 1.0;
+    const PeerBufs& P = A.peers[dest];
+    const int b = A.out_set;
+    const uint32_t slot = atomicAdd(&P.count[b][key], 1u);
+    if (slot < A.cap) {
+      store_rec(P.reg[b], (uint64_t)key * A.cap + slot, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
+    } else {  // the owner's cell is full: its overflow list
+      const uint32_t q = atomicAdd(&P.small[4 + b], 1u);
+      if (q < A.ovf_cap) {
+        store_rec(P.ovf[b], q, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
+        P.ovf_cell[b][q] = key;
+      } else {
+        atomicOr(&P.small[2], 1u);
+      }
+    }
+    return;
+  }
   const unsigned act = __ballot_sync(0xffffffffu, active);
   if (!active) return;
+  migrated += 1.0;
   const int lane = threadIdx.x & 31;
   const unsigned grp = __match_any_sync(act, dest);
   const int leader = __ffs(grp) - 1;
@@ -323,7 +362,8 @@ __device__ __forceinline__ void send_foreign(const StepArgs& A, bool active, int
 // Unbatched variant for the dense kernel.
 template <bool UNIT, int MODE>
 __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, double ny,
-                                     double nz, uint32_t id, const double* w, double m) {
+                                     double nz, uint32_t id, const double* w, double m,
+                                     double& migrated) {
   const double o[6] = {nx, ny, nz, w[0], w[1], w[2]};
   if (MODE == kById) {
     if (active) store_rec(A.out, id, nx, ny, nz, id, w[0], w[1], w[2], m);
@@ -334,7 +374,7 @@ __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, 
   if (MODE == kMulti) {
     int dest = 0;
     if (active) local = next_cell_multi<UNIT>(A, nx, ny, nz, key, dest);
-    send_foreign(A, active && !local, dest, o, id, m);
+    send_foreign(A, active && !local, dest, key, o, id, m, migrated);
   } else if (active) {
     key = next_cell<UNIT>(A, nx, ny, nz);
   }
@@ -456,7 +496,7 @@ struct StepSmem {
   TileBuf buf[kStages];
   WarpScratch w[kNCW];
   double post[DRIFT ? kTC * 4 : 1];
-  double red[kNCW * 5];
+  double red[kNCW * kDiagCols];
   uint64_t full[kStages], empty[kStages];
 };
 
@@ -609,7 +649,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       const double c = (comp < 3) ? ((mass > 0.0) ? mom / mass : 0.0)
                                   : (double)T.cnt[cw0 + q];
       if (comp < 3) W.com[q * 3 + comp] = c;
-      else acc[4] += mass;
+      else {
+        acc[4] += mass;
+        acc[5] += (double)T.cnt[cw0 + q];  // particles collided
+      }
       if (COM) A.com_cap[(c0 + cw0 + q) * 4 + comp] = c;
     }
   }
@@ -667,7 +710,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       base[r] = 0u;
       if (j0 + 32 * r < j1) {  // warp-uniform: every lane takes part in the ballot
         if (MODE == kMulti)
-          send_foreign(A, real[r] && !stay[r], dest[r], o[r], pid[r], mm[r]);
+          send_foreign(A, real[r] && !stay[r], dest[r], key[r], o[r], pid[r], mm[r], acc[6]);
         claim_slot(A, stay[r], key[r], grp[r], base[r]);
       }
     }
@@ -743,7 +786,8 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   // ------------------------------------------------------------ consumers
   WarpScratch& W = S.w[warp];
   const int cw0 = warp * kCW;  // this warp's first cell of every tile
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // px py pz sum(m v^2) mass
+  // px py pz sum(m v^2) mass, particles collided, particles sent to other ranks
+  double acc[kDiagCols] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int64_t tile = blockIdx.x;
   for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
     const int b = (int)(i % kStages);
@@ -774,17 +818,20 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     }
     if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
   }
+  // fused migration: this thread's stores into peers' regions become visible
+  // system-wide before the step fence (the all-reduce that follows the step)
+  if (A.peers) __threadfence_system();
   // CTA partials: fixed-order block reduction of the per-thread sums
 #pragma unroll
-  for (int q = 0; q < 5; ++q)
+  for (int q = 0; q < kDiagCols; ++q)
     for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
   if (lane == 0)
 #pragma unroll
-    for (int q = 0; q < 5; ++q) S.red[warp * 5 + q] = acc[q];
+    for (int q = 0; q < kDiagCols; ++q) S.red[warp * kDiagCols + q] = acc[q];
   consumer_sync();
-  if (t < 5) {
+  if (t < kDiagCols) {
     double s = 0.0;
-    for (int w = 0; w < kNCW; ++w) s += S.red[w * 5 + t];
+    for (int w = 0; w < kNCW; ++w) s += S.red[w * kDiagCols + t];
     A.partials[(int64_t)blockIdx.x * 8 + t] = s;
   }
 }
@@ -806,7 +853,9 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
   const int t = threadIdx.x;
   const uint32_t n_dense = *(volatile uint32_t*)&A.flags[0];
   const uint32_t n_ovf = min(*(volatile uint32_t*)A.ovf_n_in, A.ovf_cap);
-  double dacc = 0.0;  // thread t < 5: this CTA's partial sum of column t
+  double dacc = 0.0;  // thread t < kDiagCols: this CTA's partial sum of column t
+  double dmig = 0.0;  // this thread's particles sent to other ranks
+  __shared__ double s_mig[kNT / 32];
   for (uint32_t e = blockIdx.x; e < n_dense; e += gridDim.x) {
     const int64_t tile = A.dense[e];  // sorted by k_sort_dense: deterministic sums
     const int64_t c0 = tile * kTC;
@@ -918,7 +967,7 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
         g_val[4 * s] = m * w[0]; g_val[4 * s + 1] = m * w[1]; g_val[4 * s + 2] = m * w[2];
         g_val[4 * s + 3] = m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]);
       }
-      emit<UNIT, MODE>(A, active, nx, ny, nz, id, w, UMASS ? A.m0 : m);
+      emit<UNIT, MODE>(A, active, nx, ny, nz, id, w, UMASS ? A.m0 : m, dmig);
     }
     __syncthreads();
     for (int task = t; task < nc * 4; task += kNT) {
@@ -926,8 +975,9 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       s_post[task] = s_cnt[lc] ? reduceat(g_val + 4 * (uint64_t)s_off[lc] + comp, (int64_t)s_cnt[lc], 4) : 0.0;
     }
     __syncthreads();
-    if (t < 5)
-      for (int lc = 0; lc < nc; ++lc) dacc += (t < 4) ? s_post[lc * 4 + t] : s_mom[lc * 4 + 3];
+    if (t < 6)
+      for (int lc = 0; lc < nc; ++lc)
+        dacc += (t < 4) ? s_post[lc * 4 + t] : (t == 4 ? s_mom[lc * 4 + 3] : (double)s_cnt[lc]);
     if (DRIFT && t >= 32 && t < 64) {
       double worst = 0.0;
       for (int lc = t - 32; lc < nc; lc += 32)
@@ -937,7 +987,13 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
     }
     if (t < nc) A.count_in[c0 + t] = 0u;
   }
-  if (t < 5) A.partials[(A.part_base + blockIdx.x) * 8 + t] = dacc;
+  if (A.peers) __threadfence_system();
+  for (int o = 16; o > 0; o >>= 1) dmig += __shfl_xor_sync(0xffffffffu, dmig, o);
+  if ((t & 31) == 0) s_mig[t >> 5] = dmig;
+  __syncthreads();
+  if (t == 6)
+    for (int w = 0; w < kNT / 32; ++w) dacc += s_mig[w];
+  if (t < kDiagCols) A.partials[(A.part_base + blockIdx.x) * 8 + t] = dacc;
 }
 
 // The dense-tile list is appended in arbitrary order; sort it (ascending) so
@@ -958,42 +1014,52 @@ constexpr int kDiagBlocks = 592;
 
 __global__ void __launch_bounds__(256) k_diag_partial(const double* partials, int64_t ntiles,
                                                      double* level1) {
-  __shared__ double s[5][256];
+  __shared__ double s[kDiagCols][256];
   const int t = threadIdx.x;
   const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(ntiles, lo + per);
-  double acc[5] = {0, 0, 0, 0, 0};
+  double acc[kDiagCols] = {0, 0, 0, 0, 0, 0, 0};
   for (int64_t i = lo + t; i < hi; i += 256)
 #pragma unroll
-    for (int c = 0; c < 5; ++c) acc[c] += partials[i * 8 + c];
+    for (int c = 0; c < kDiagCols; ++c) acc[c] += partials[i * 8 + c];
 #pragma unroll
-  for (int c = 0; c < 5; ++c) s[c][t] = acc[c];
+  for (int c = 0; c < kDiagCols; ++c) s[c][t] = acc[c];
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     if (t < w)
 #pragma unroll
-      for (int c = 0; c < 5; ++c) s[c][t] += s[c][t + w];
+      for (int c = 0; c < kDiagCols; ++c) s[c][t] += s[c][t + w];
     __syncthreads();
   }
-  if (t < 5) level1[blockIdx.x * 5 + t] = s[t][0];
+  if (t < kDiagCols) level1[blockIdx.x * kDiagCols + t] = s[t][0];
 }
 
-// Final fixed-order sum; also retires the step's transient counters.
+// Final fixed-order sum (strided lanes, then a shuffle tree); also retires the
+// step's transient counters.  out: px py pz energy mass drift n step migrated.
 __global__ void __launch_bounds__(32) k_diag_finalize(const double* level1, int nblocks,
                                                      unsigned long long* drift_bits, double* out,
-                                                     int64_t n, int64_t step, uint32_t* flags,
+                                                     int64_t step, uint32_t* flags,
                                                      uint32_t* ovf_n_consumed,
                                                      uint32_t* scratch_n) {
   const int t = threadIdx.x;
-  if (t < 5) {
+  double col[kDiagCols];
+#pragma unroll
+  for (int c = 0; c < kDiagCols; ++c) {
     double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += level1[b * 5 + t];
-    out[t] = (t == 3) ? 0.5 * s : s;
+    for (int b = t; b < nblocks; b += 32) s += level1[b * kDiagCols + c];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    col[c] = s;
   }
   if (t == 0) {
+    out[0] = col[0];
+    out[1] = col[1];
+    out[2] = col[2];
+    out[3] = 0.5 * col[3];
+    out[4] = col[4];
     out[5] = __longlong_as_double((long long)*drift_bits);
-    out[6] = (double)n;
+    out[6] = col[5];
     out[7] = (double)step;
+    out[8] = col[6];
     *drift_bits = 0ULL;
     flags[0] = 0u;         // dense-tile list consumed
     *ovf_n_consumed = 0u;  // this step's input overflow list consumed

@@ -17,6 +17,20 @@ another rank into a per-destination send buffer; the runner exchanges counts
 (one all_gather of the P x P count matrix), then the records (grouped
 point-to-point), and ``mpcd_absorb`` bins the received ones.
 
+Two migration modes:
+
+* ``"fused"`` (default, the B200 path): after the domains connect their
+  region / count / overflow allocations (CUDA IPC handles between
+  processes, direct pointers within one), ``k_step`` itself writes each
+  leaving particle into its new owner's next-step cell -- slot claimed by an
+  atomic on the owner's count, record stored over NVLink peer memory.  A step
+  is one kernel per rank plus a one-element all-reduce enqueued on the stream
+  as the step fence; no send buffers, no host synchronisation, no absorb.
+* ``"exchange"``: the particles go to per-destination send buffers; the
+  runner all-gathers the count matrix and moves the records with grouped
+  point-to-point sends (NCCL, or gloo host-staged), and ``mpcd_absorb`` bins
+  them.  Also the fallback when peer memory cannot be opened.
+
 The exchange is written against a small ``Domain`` interface (``step``,
 ``send_counts``, ``send_view``, ``absorb``, ``diag``) so the same host logic
 drives the CUDA domains and, in the CPU test-suite, a model domain.
@@ -35,6 +49,7 @@ from .params import SimParams
 from .particles import ParticleSet, init_system
 
 RECORD_BYTES = 64  # x y z id|pad vx vy vz m (include/mpcd.h, mpcd_exchange)
+MIGRATIONS = ("fused", "exchange")
 
 
 # ------------------------------------------------------------------ layout --
@@ -102,6 +117,9 @@ def _check_overflow(counts: np.ndarray, cap: int):
 class LocalExchange:
     """Every domain in this process: the records move by device copies."""
 
+    def fence(self):
+        pass  # one stream: domain steps run in order
+
     def exchange(self, domains) -> list:
         import torch
 
@@ -134,6 +152,22 @@ class DistExchange:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.host_staged = dist.get_backend(group) != "nccl"
+        self._token = None
+
+    def fence(self):
+        """Step fence of the fused migration: every rank's step k completes
+        before any rank's step k+1 starts.  NCCL: a one-element all-reduce on
+        the current stream (device-side ordering, no host wait); gloo: the
+        host waits for the device, then a barrier."""
+        import torch
+
+        if self.host_staged:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+            return
+        if self._token is None:
+            self._token = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.dist.all_reduce(self._token, group=self.group)
 
     def _stage(self, t):
         return t.cpu() if self.host_staged else t
@@ -245,7 +279,8 @@ class CudaDomain:
 
     def diag(self):
         d = self.ctx.read_diag()
-        return np.array([*d.momentum, d.energy, d.mass, d.max_cell_drift, self.ctx.n, d.step])
+        return np.array([*d.momentum, d.energy, d.mass, d.max_cell_drift, d.n, d.step,
+                         d.migrated])
 
     def read_com(self):
         return self.ctx.read_com()
@@ -267,7 +302,7 @@ class CudaDomain:
 def _merge(diags: list, crossings: int) -> dict:
     """Per-rank diagnostics combined in rank order (runners.py:27-56)."""
     out = {"n": 0, "momentum": np.zeros(3), "energy": 0.0, "mass": 0.0,
-           "crossings": int(crossings)}
+           "crossings": int(crossings)}  # particles that changed domain
     for d in diags:
         out["n"] += int(d[6])
         out["momentum"] = out["momentum"] + d[0:3]
@@ -285,10 +320,11 @@ class _DomainRunner:
     """Runner duck type of the reference (runners.py:73-155) over domains."""
 
     def __init__(self, params: SimParams, domains: list, exchange, *, capture_drift: bool,
-                 capture_com: bool):
+                 capture_com: bool, fused: bool = False):
         self.params = params
         self.domains = domains
         self.exchange = exchange
+        self.fused = fused
         self.capture_drift = capture_drift
         self.capture_com = capture_com
         self.transport = None
@@ -304,6 +340,9 @@ class _DomainRunner:
         f = self._flags() if flags is None else flags
         for d in self.domains:
             d.step(k, f)
+        if self.fused:  # the particles already moved inside k_step
+            self.exchange.fence()
+            return 0
         return sum(self.exchange.exchange(self.domains))
 
     def _gather(self, obj):
@@ -312,12 +351,11 @@ class _DomainRunner:
         return [obj]
 
     def run_step(self, step: int) -> dict:
-        sent = self.advance(step)
+        self.advance(step)
         local = [(d.rank, d.diag(), d.read_com() if self.capture_com else None)
                  for d in self.domains]
-        groups = self._gather((sent, local))
-        parts = sorted((x for g in groups for x in g[1]), key=lambda x: x[0])
-        diag = _merge([p[1] for p in parts], sum(g[0] for g in groups))
+        parts = sorted((x for g in self._gather(local) for x in g), key=lambda x: x[0])
+        diag = _merge([p[1] for p in parts], int(sum(p[1][8] for p in parts)))
         if self.capture_drift:
             diag["max_cell_drift"] = max(float(p[1][5]) for p in parts)
         if self.capture_com:
@@ -375,17 +413,24 @@ class SequentialRunner(_DomainRunner):
 
     def __init__(self, params: SimParams, *, policy: str = "immediate",
                  capture_drift: bool = False, capture_com: bool = False,
-                 velocity_variance: float = 1.0, init: str = "host", send_capacity: int = 0):
+                 velocity_variance: float = 1.0, init: str = "host", send_capacity: int = 0,
+                 migration: str = "fused"):
         # `policy` (immediate / lazy migration, engine.py:134-146) trades halo
         # width against migration traffic in the reference; with cell
         # ownership every step migrates exactly the particles that change
         # owner, so both policies run the same exchange.
         layout = DomainLayout.from_params(params)
+        if migration not in MIGRATIONS:
+            raise ConfigError(f"migration must be one of {MIGRATIONS}")
         domains = [CudaDomain(params, layout, r, send_capacity=send_capacity)
                    for r in range(layout.n_ranks)]
+        fused = migration == "fused"
+        if fused:
+            from .engine import EngineContext
+            EngineContext.connect_local([d.ctx for d in domains])
         _initialise(domains, params, velocity_variance, init)
         super().__init__(params, domains, LocalExchange(), capture_drift=capture_drift,
-                         capture_com=capture_com)
+                         capture_com=capture_com, fused=fused)
         self.layout = layout
 
 
@@ -419,9 +464,11 @@ class NcclRunner(_DomainRunner):
     def __init__(self, params: SimParams, *, policy: str = "immediate",
                  capture_drift: bool = False, capture_com: bool = False,
                  velocity_variance: float = 1.0, init: str = "host", send_capacity: int = 0,
-                 group=None, domain_factory=None):
+                 group=None, domain_factory=None, migration: str = "fused"):
         import torch.distributed as dist
 
+        if migration not in MIGRATIONS:
+            raise ConfigError(f"migration must be one of {MIGRATIONS}")
         layout = DomainLayout.from_params(params)
         if not dist.is_initialized():
             init_distributed("nccl")
@@ -430,11 +477,37 @@ class NcclRunner(_DomainRunner):
             raise ConfigError(f"backend nccl runs one domain per process: rank_dims "
                               f"{params.rank_dims} needs {layout.n_ranks} processes, got {world}")
         rank = dist.get_rank(group)
+        exchange = DistExchange(group)
         if domain_factory is None:
             domains = [CudaDomain(params, layout, rank, send_capacity=send_capacity)]
+            fused = migration == "fused" and connect_fused(domains[0], exchange)
         else:
             domains = [domain_factory(params, layout, rank)]
+            fused = False
         _initialise(domains, params, velocity_variance, init)
-        super().__init__(params, domains, DistExchange(group), capture_drift=capture_drift,
-                         capture_com=capture_com)
+        super().__init__(params, domains, exchange, capture_drift=capture_drift,
+                         capture_com=capture_com, fused=fused)
         self.layout = layout
+        self.migration = "fused" if fused else "exchange"
+
+
+def connect_fused(dom: "CudaDomain", exchange: DistExchange) -> bool:
+    """Open every other rank's regions (CUDA IPC) for the fused migration.
+    All ranks agree: if any rank fails, all fall back to the exchange."""
+    err = None
+    try:
+        handles = dom.ctx.ipc_handles()
+    except Exception as e:  # noqa: BLE001 - reported, then the fallback
+        err, handles = repr(e), b""
+    allh = exchange.gather_objects(handles)
+    if err is None and all(allh):
+        try:
+            dom.ctx.connect_peers(b"".join(allh), exchange.world)
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)
+    errs = [e for e in exchange.gather_objects(err) if e]
+    if errs:
+        import warnings
+        warnings.warn(f"fused migration unavailable ({errs[0]}); using the exchange path")
+        return False
+    return True

@@ -160,6 +160,26 @@ class EngineContext:
         self.exchange_info = ex
         return ex
 
+    def ipc_handles(self) -> bytes:
+        """CUDA IPC handles of this context's regions, counts and overflow lists."""
+        n = C.c_int64(0)
+        _lib.check(self._lib.mpcd_ipc_handles(self.handle, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _lib.check(self._lib.mpcd_ipc_handles(self.handle, buf, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def connect_peers(self, all_handles: bytes, n_ranks: int):
+        """Fused migration over peer memory opened from every rank's handles."""
+        buf = C.create_string_buffer(all_handles, len(all_handles))
+        _lib.check(self._lib.mpcd_connect_peers(self.handle, buf, int(n_ranks)))
+
+    @staticmethod
+    def connect_local(ctxs):
+        """Fused migration between the domains of this process (ctxs[rank])."""
+        lib = _lib.load()
+        arr = (C.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+        _lib.check(lib.mpcd_connect_local(arr, len(ctxs)))
+
     def absorb(self, recv_ptr: int, n_recv: int, n_sent: int):
         _lib.check(self._lib.mpcd_absorb(self.handle, C.c_void_p(int(recv_ptr) or None),
                                          int(n_recv), int(n_sent), _dev.stream()))
@@ -307,7 +327,7 @@ class Simulation:
     def __init__(self, params: SimParams, *, backend: str = BACKEND_CUDA,
                  policy: str = POLICY_IMMEDIATE, capture_drift: bool = False,
                  capture_com: bool = False, velocity_variance: float = 1.0,
-                 init: str = "host"):
+                 init: str = "host", migration: str = "fused"):
         if policy not in POLICIES:
             raise ConfigError(f"migration policy must be one of {POLICIES}")
         self.params = params
@@ -330,7 +350,7 @@ class Simulation:
             cls = NcclRunner if backend == BACKEND_NCCL else SequentialRunner
             self._runner = cls(params, policy=policy, capture_drift=capture_drift,
                                capture_com=capture_com, velocity_variance=velocity_variance,
-                               init=init)
+                               init=init, migration=migration)
         else:
             raise ConfigError(f"unknown backend {backend!r}")
 

@@ -82,6 +82,7 @@ class ModelDomain:
             rec["vx"], rec["vy"], rec["vz"] = r.velocities[sel].T
             rec["m"] = 1.0
         stay = dest == self.rank
+        self.collided, self.migrated = len(self.ids), int((~stay).sum())
         self.ids, self.pos, self.vel = self.ids[stay], r.positions[stay], r.velocities[stay]
         self.k = k + 1
 
@@ -107,7 +108,7 @@ class ModelDomain:
 
     def diag(self):
         d = oracle.diag(self.post_vel, np.ones(len(self.post_vel)))
-        return np.array([*d[:3], d[3], d[4], 0.0, len(self.ids), self.k - 1])
+        return np.array([*d[:3], d[3], d[4], 0.0, self.collided, self.k - 1, self.migrated])
 
     def read_com(self):
         raise NotImplementedError

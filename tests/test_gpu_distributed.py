@@ -46,11 +46,12 @@ def run(params, backend, n_steps, **kw):
     ((8, 8, 8), (8, 1, 1)),     # one-cell slabs: most particles change owner every step
     ((4, 4, 4), (2, 2, 4)),     # 1-2 cells per domain axis, 16 domains
 ])
-def test_sequential_domains_bitwise_equal_whole_box(dims, rank_dims):
+@pytest.mark.parametrize("migration", ["fused", "exchange"])
+def test_sequential_domains_bitwise_equal_whole_box(dims, rank_dims, migration):
     base = mp.SimParams(edge_length=dims[0], edge_lengths=dims, seed=11)
     dec = mp.SimParams(edge_length=dims[0], edge_lengths=dims, seed=11, rank_dims=rank_dims)
     ids_a, pa, da, ca, _ = run(base, "cuda", 6, capture_com=True)
-    ids_b, pb, db, cb, _ = run(dec, "sequential", 6, capture_com=True)
+    ids_b, pb, db, cb, _ = run(dec, "sequential", 6, capture_com=True, migration=migration)
     assert np.array_equal(ids_a, ids_b)
     assert np.array_equal(pa.positions, pb.positions)
     assert np.array_equal(pa.velocities, pb.velocities)
@@ -98,7 +99,7 @@ def test_device_init_domains_equal_whole_box(prng):
 def test_migration_overflow_raises():
     params = mp.SimParams(edge_length=16, seed=1, rank_dims=(2, 1, 1))
     from paper_2212_11878_b200.distributed import SequentialRunner
-    r = SequentialRunner(params, send_capacity=8)
+    r = SequentialRunner(params, send_capacity=8, migration="exchange")
     try:
         with pytest.raises(mp.MpcdError, match="overflow"):
             r.run_step(0)
@@ -125,7 +126,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, migration):
     import torch
     import torch.distributed as dist
 
@@ -134,20 +135,27 @@ def _worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         params = mp.SimParams(edge_length=16, seed=4, rank_dims=(world, 1, 1))
-        with mp.Simulation(params, backend="nccl", capture_com=True) as sim:
+        with mp.Simulation(params, backend="nccl", capture_com=True,
+                           migration=migration) as sim:
             diags = [sim.step() for _ in range(4)]
             ids, p = sim.collect()
             ci, cv = sim.com_captures[-1]
+            used = sim.runner.migration
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids, pos=p.positions,
-                 vel=p.velocities, ci=ci, cv=cv, crossings=[d["crossings"] for d in diags])
+                 vel=p.velocities, ci=ci, cv=cv, crossings=[d["crossings"] for d in diags],
+                 used=used)
     finally:
         dist.destroy_process_group()
 
 
-def test_two_processes_gloo_equal_whole_box(tmp_path):
+@pytest.mark.parametrize("migration", ["fused", "exchange"])
+def test_two_processes_gloo_equal_whole_box(tmp_path, migration):
+    """Two processes sharing one GPU: fused = k_step writes into the other
+    process's regions through CUDA IPC handles; exchange = gloo host-staged."""
     import torch.multiprocessing as tmp_mp
 
-    tmp_mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    tmp_mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), migration), nprocs=2,
+                 join=True)
     params = mp.SimParams(edge_length=16, seed=4)
     ids, p, _, coms, _ = run(params, "cuda", 4, capture_com=True)
     for r in range(2):
@@ -157,3 +165,4 @@ def test_two_processes_gloo_equal_whole_box(tmp_path):
         assert np.array_equal(o["vel"], p.velocities)
         assert np.array_equal(o["ci"], coms[-1][0]) and np.array_equal(o["cv"], coms[-1][1])
         assert np.all(o["crossings"] > 0)
+        assert str(o["used"]) == migration
