@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--cpu-sample-L", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--migration", default="fused", choices=("fused", "exchange"),
+                    help="N > 1: particle migration inside k_step over peer memory, or "
+                         "through send buffers + NCCL point-to-point")
     return ap.parse_args()
 
 
@@ -224,28 +227,35 @@ def run_ours(args):
                             params.prng, n, mass_value=1.0)
         ctx.init_device(n, 1.0, 0)
         n_total = n
+        fused = False
 
         def run_steps(first, count):
             ctx.run(first, count)  # no host synchronisation between steps
     else:
         # BASELINE config 4: (L*ws) x L x L box, slab-decomposed, L^3 cells per
-        # GPU, particle migration over NCCL every step
-        from paper_2212_11878_b200.distributed import CudaDomain, DistExchange, DomainLayout
+        # GPU.  Fused migration: k_step writes leaving particles into the
+        # neighbour's cells over NVLink peer memory, a one-element NCCL
+        # all-reduce fences each step (falls back to the NCCL exchange if
+        # peer memory cannot be opened).
+        from paper_2212_11878_b200.distributed import (CudaDomain, DistExchange, DomainLayout,
+                                                       _DomainRunner, connect_fused)
         dims = (L * ws, L, L)
         params = SimParams(edge_length=dims[0], edge_lengths=dims, seed=args.seed,
                            rank_dims=(ws, 1, 1))
         layout = DomainLayout.from_params(params)
         dom = CudaDomain(params, layout, rank)
+        exch = DistExchange()
+        fused = args.migration == "fused" and connect_fused(dom, exch)
         dom.init_device(params.n_particles, 1.0)
         ctx = dom.ctx
-        exch = DistExchange()
+        runner_md = _DomainRunner(params, [dom], exch, capture_drift=False, capture_com=False,
+                                  fused=fused)
         n_total = params.n_particles
         n = n_total // ws
 
         def run_steps(first, count):
             for k in range(first, first + count):
-                dom.step(k, 0)
-                exch.exchange([dom])
+                runner_md.advance(k, 0)
     C = L ** 3
     run_steps(0, args.warmup)
     torch.cuda.synchronize()
@@ -313,7 +323,9 @@ def run_ours(args):
                    "cells_per_gpu": C, "particles_per_gpu": n,
                    "parallelism": "single domain" if ws == 1 else
                    f"slab decomposition ({ws},1,1) of a {L * ws}x{L}x{L} box (BASELINE "
-                   "config 4), particle migration over NCCL every step",
+                   "config 4), particle migration every step: " +
+                   ("fused into k_step over NVLink peer memory, NCCL all-reduce step fence"
+                    if ws > 1 and fused else "send buffers + NCCL point-to-point"),
                    "l2": "state 17 GB >> 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -331,14 +343,14 @@ def run_ours(args):
             "survey_b_alg_frac": survey_bytes / (ms * 1e-3) / 1e9 / peak,
             "b_min_frac": B_MIN_N * n / (ms * 1e-3) / 1e9 / peak,
             "kernel_ms": per_kernel},
-        "gpu_launches": args.steps * (LAUNCHES_PER_STEP + (1 if ws > 1 else 0)),
+        "gpu_launches": args.steps * (LAUNCHES_PER_STEP + (1 if ws > 1 and not fused else 0)),
         "diag_last": {"momentum": list(d.momentum), "energy": d.energy, "mass": d.mass},
     }
     line["clocks"] = clocks.summary()
     if ws == 1 and not args.no_e2e:
         line["e2e"], line["e2e_stateful"] = e2e(args, params, ctx)
     elif ws > 1 and not args.no_e2e:
-        line["e2e"] = e2e_decomposed(args, params, dom, exch)
+        line["e2e"] = e2e_decomposed(args, params, dom, exch, fused)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.cpu_sample_L, 3, args.seed)
     if rank == 0:
@@ -348,14 +360,15 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
-def e2e_decomposed(args, params, dom, exch):
+def e2e_decomposed(args, params, dom, exch, fused):
     """Simulation.step() of the nccl backend (NcclRunner.run_step): step,
     migration, per-rank diagnostics read back and merged on every rank."""
     import torch
 
     from paper_2212_11878_b200.distributed import _DomainRunner
 
-    runner = _DomainRunner(params, [dom], exch, capture_drift=False, capture_com=False)
+    runner = _DomainRunner(params, [dom], exch, capture_drift=False, capture_com=False,
+                           fused=fused)
     first = int(dom.ctx._lib.mpcd_current_step(dom.ctx.handle))  # a domain steps consecutively
     runner.run_step(first)
     torch.cuda.synchronize()
