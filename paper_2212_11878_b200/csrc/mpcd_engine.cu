@@ -1431,3 +1431,18 @@ void mpcd_grid_shift(int32_t prng, uint64_t seed, uint64_t step, double cell_siz
 }
 
 }  // extern "C"
+
+#ifdef MPCD_TIMING
+// Tuning builds only (-DMPCD_TIMING): per-phase clock64 sums of the k_step
+// consumer warps (tools/phase_timing.py).
+extern "C" int mpcd_debug_phase_cycles(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, mpcd::g_phase_cycles, sizeof(unsigned long long) * 10) !=
+      cudaSuccess)
+    return MPCD_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[10] = {0};
+    cudaMemcpyToSymbol(mpcd::g_phase_cycles, z, sizeof(z));
+  }
+  return MPCD_OK;
+}
+#endif

@@ -50,9 +50,51 @@ __device__ __forceinline__ uint32_t bits_id(double d) {
 __device__ __forceinline__ double2 ld2cs(const void* p) {  // read-once stream
   return __ldcs(reinterpret_cast<const double2*>(p));
 }
+// Record stores stream past L2 (evict-first): the step writes ~11 GB of
+// records at 256^3 that are only read back next step from DRAM, and must not
+// evict the next-step count array whose slot atomics sit on the critical path.
+#ifndef MPCD_STCS
+#define MPCD_STCS 1
+#endif
 __device__ __forceinline__ void st2(void* p, double a, double b) {
-  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+  if (MPCD_STCS)
+    __stcs(reinterpret_cast<double2*>(p), make_double2(a, b));
+  else
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
+// Next-step counts stay in L2 (evict-last): their slot atomics are on the
+// critical path of every particle, and 40 % of them missed L2 with default
+// priority while the step streams its records through it.
+#ifndef MPCD_PREFETCH_COUNTS
+#define MPCD_PREFETCH_COUNTS 0  // measured slower (7.55 vs 7.40 ms): off
+#endif
+#ifndef MPCD_CNT_EVICT_LAST
+#define MPCD_CNT_EVICT_LAST 1
+#endif
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint32_t count_claim(uint32_t* p, uint32_t v) {
+  if (!MPCD_CNT_EVICT_LAST) return atomicAdd(p, v);
+  uint32_t old;
+  asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], %2, %3;"
+               : "=r"(old)
+               : "l"(p), "r"(v), "l"(policy_evict_last())
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void count_zero(uint32_t* p) {
+  if (!MPCD_CNT_EVICT_LAST) {
+    *p = 0u;
+    return;
+  }
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(0u),
+               "l"(policy_evict_last())
+               : "memory");
+}
+
 __device__ __forceinline__ void store_rec(const Recs& s, uint64_t dst, double x, double y,
                                           double z, uint32_t id, double vx, double vy, double vz,
                                           double m) {
@@ -281,7 +323,7 @@ __device__ __forceinline__ void claim_slot(const StepArgs& A, bool active, uint3
   grp = 0u;
   base = 0u;
   if (MPCD_NOAGG) {  // one atomic per particle: the slot itself
-    if (active) base = atomicAdd(&A.count_out[key], 1u);
+    if (active) base = count_claim(&A.count_out[key], 1u);
     return;
   }
   const unsigned act = __ballot_sync(0xffffffffu, active);
@@ -442,6 +484,20 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+#ifdef MPCD_TIMING
+__device__ unsigned long long g_phase_cycles[10];
+__device__ unsigned long long g_wait_cycles;
+#define MPCD_PROBE(k)                                                              \
+  do {                                                                             \
+    const long long now_ = clock64();                                              \
+    if ((k) > 0 && (threadIdx.x & 31) == 0)                                        \
+      atomicAdd(&g_phase_cycles[(k)], (unsigned long long)(now_ - probe_t_));      \
+    probe_t_ = now_;                                                               \
+  } while (0)
+#else
+#define MPCD_PROBE(k) do {} while (0)
+#endif
+
 // ------------------------------------------------------- the step kernel --
 // Persistent and warp-specialised.  CTA b walks tiles b, b + G, ...  The
 // producer warp prepares tiles ahead of the consumers: reads the tile's
@@ -567,7 +623,24 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
     bulk_load(B.p + excl, A.in.p + src, bytes, full, pol);
     bulk_load(B.v + excl, A.in.v + src, bytes, full, pol);
   }
-  if (lane < nc) A.count_in[c0 + lane] = 0u;  // consumed: the count_out of step k+1
+  if (lane < nc) count_zero(&A.count_in[c0 + lane]);  // consumed: the count_out of step k+1
+#if MPCD_PREFETCH_COUNTS
+  // The tile's particles claim slots in next-step cells within one cell of
+  // their own: pull those count lines into L2 now, a tile ahead of the
+  // claims (9 (x, y) rows x the tile's z-range +- 1, two 128 B lines each).
+  if (lane < 18 && nc > 0) {
+    const int64_t zyx = c0 / A.L2;  // x * L1 + y of the tile (tiles do not cross z rows)
+    const int z0 = (int)(c0 - zyx * A.L2);
+    const int x = (int)(zyx / A.L1), y = (int)(zyx - (int64_t)x * A.L1);
+    const int r = lane >> 1;
+    int xn = x + r / 3 - 1, yn = y + r % 3 - 1;
+    xn = xn < 0 ? xn + A.L0 : (xn >= A.L0 ? xn - A.L0 : xn);
+    yn = yn < 0 ? yn + A.L1 : (yn >= A.L1 ? yn - A.L1 : yn);
+    const int zn = (lane & 1) ? min(z0 + nc, A.L2 - 1) : max(z0 - 1, 0);
+    const uint32_t* q = A.count_out + ((int64_t)xn * A.L1 + yn) * A.L2 + zn;
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(q));
+  }
+#endif
   for (uint32_t j = excl; j < incl; ++j) B.cell[j] = (uint8_t)lane;
   // rotation axes (collision.py:217-250), keyed by the global cell id
   if (lane < kTC) {
@@ -587,6 +660,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
                                               int ncw, int j0, int j1, double* acc) {
   constexpr bool BYID = MODE == kById;
   const int lane = threadIdx.x & 31;
+#ifdef MPCD_TIMING
+  long long probe_t_ = 0;
+#endif
+  MPCD_PROBE(0);
 
   // phase 1: ids in slot order (sentinel in the padding), warp-local rows
   int lq[R];  // cell of the row inside the warp (0..3)
@@ -604,6 +681,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
+  MPCD_PROBE(1);
 
   // phase 2: rank by id inside the cell, 4-wide over the padded segment;
   // stage (m v, m) in rank order -- the reference permutation is the stable
@@ -631,6 +709,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
+  MPCD_PROBE(2);
 
   // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206);
   // four lanes per cell, com = p / m (collision.py:209-214) from the group's
@@ -657,6 +736,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
+  MPCD_PROBE(3);
 
   // phase 4: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
   // next-step cell; claim every slot, then store; stage post-collision rows
@@ -716,6 +796,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
+  MPCD_PROBE(4);
 
   // phase 5: conservation sums over the staged post rows, each lane its
   // rank positions (fixed: deterministic) -- while the slot claims are in
@@ -730,6 +811,16 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
     }
   }
+  MPCD_PROBE(5);
+#ifdef MPCD_TIMING
+  {  // wait for the claims alone
+    uint32_t dep = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dep += base[r];
+    if (dep == 0xFFFFFFFFu) acc[0] += 1.0;
+  }
+  MPCD_PROBE(6);
+#endif
   if (!BYID) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -752,6 +843,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
     if (lane == 0 && worst > 0.0) atomic_max_pos_double(A.drift_bits, worst);
   }
+  MPCD_PROBE(7);
 }
 
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
@@ -792,7 +884,14 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
     const int b = (int)(i % kStages);
     TileBuf& T = S.buf[b];
+#ifdef MPCD_TIMING
+    const long long tw0 = clock64();
+#endif
     mbar_wait(&S.full[b], (uint32_t)(i / kStages) & 1u);
+#ifdef MPCD_TIMING
+    if (lane == 0) atomicAdd(&g_phase_cycles[8], (unsigned long long)(clock64() - tw0));
+    if (lane == 0) atomicAdd(&g_phase_cycles[9], 1ull);
+#endif
     const int64_t c0 = tile * kTC;
     const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)kCW, A.C - c0 - cw0));
     if (ncw == 0) {
