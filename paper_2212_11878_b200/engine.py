@@ -472,8 +472,12 @@ def _build_for_check(params, rank_dims, scheme, capture_com, backend):
 
 def equivalence_check(config: SimParams, ranks_a, ranks_b, scheme_a: str, scheme_b: str,
                       n_steps: int, *, capture_com: bool = False,
-                      backend: str = BACKEND_NCCL) -> EquivalenceReport:
-    """Run two settings of one physical config in lockstep (engine.py:703-748)."""
+                      backend: str = BACKEND_SEQUENTIAL) -> EquivalenceReport:
+    """Run two settings of one physical config in lockstep (engine.py:703-748).
+
+    The reference's default backend is its in-process "sequential" runner;
+    here "sequential" runs the decomposed box's domains in-process on one GPU.
+    """
     box = config.box_lengths
     report = EquivalenceReport(n_steps=n_steps)
     sim_a = _build_for_check(config, ranks_a, scheme_a, capture_com, backend)

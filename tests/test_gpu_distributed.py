@@ -166,3 +166,16 @@ def test_two_processes_gloo_equal_whole_box(tmp_path, migration):
         assert np.array_equal(o["ci"], coms[-1][0]) and np.array_equal(o["cv"], coms[-1][1])
         assert np.all(o["crossings"] > 0)
         assert str(o["used"]) == migration
+
+
+@pytest.mark.parametrize("scheme", ["halo", "migration"])
+def test_equivalence_check_serial_vs_decomposed_is_exact(scheme):
+    """Acceptance criterion 3 of the reference (cross-scheme equivalence,
+    test_acceptance.py:63-85, bound 1e-10): here the deviations are zero."""
+    params = mp.SimParams(edge_length=12, seed=8)
+    rep = mp.equivalence_check(params, (1, 1, 1), (2, 2, 1), "serial", scheme, 5,
+                               capture_com=True)
+    assert rep.n_steps == 5
+    assert rep.max_position_dev == 0.0
+    assert rep.max_velocity_dev == 0.0
+    assert rep.max_com_dev == 0.0
