@@ -487,11 +487,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 #ifdef MPCD_TIMING
 __device__ unsigned long long g_phase_cycles[10];
 __device__ unsigned long long g_wait_cycles;
+// per-warp shared accumulators (S.tim), flushed once per warp at kernel end
 #define MPCD_PROBE(k)                                                              \
   do {                                                                             \
     const long long now_ = clock64();                                              \
     if ((k) > 0 && (threadIdx.x & 31) == 0)                                        \
-      atomicAdd(&g_phase_cycles[(k)], (unsigned long long)(now_ - probe_t_));      \
+      S.tim[threadIdx.x >> 5][(k)] += (unsigned long long)(now_ - probe_t_);       \
     probe_t_ = now_;                                                               \
   } while (0)
 #else
@@ -511,7 +512,10 @@ __device__ unsigned long long g_wait_cycles;
 // for each other.  Two tile buffers with full / empty mbarriers (empty
 // counts one arrival per consumer warp).
 constexpr int kMaxPT = MPCD_MAXPT;     // padded record slots per tile in shared memory
-constexpr int kCW = 4;                 // cells per consumer warp
+#ifndef MPCD_CW
+#define MPCD_CW 4
+#endif
+constexpr int kCW = MPCD_CW;           // cells per consumer warp
 constexpr int kNCW = kTC / kCW;        // consumer warps
 constexpr int kNC = kNCW * 32;         // consumer threads
 constexpr int kNTW = kNC + 32;         // + one producer warp
@@ -553,6 +557,9 @@ struct StepSmem {
   WarpScratch w[kNCW];
   double post[DRIFT ? kTC * 4 : 1];
   double red[kNCW * kDiagCols];
+#ifdef MPCD_TIMING
+  unsigned long long tim[kNCW][10];
+#endif
   uint64_t full[kStages], empty[kStages];
 };
 
@@ -852,6 +859,9 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t G = gridDim.x;
+#ifdef MPCD_TIMING
+  if (t < kNCW * 10) (&S.tim[0][0])[t] = 0ull;
+#endif
   if (t == 0) {
     for (int b = 0; b < kStages; ++b) {
       mbar_init(&S.full[b], 2);
@@ -889,8 +899,8 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 #endif
     mbar_wait(&S.full[b], (uint32_t)(i / kStages) & 1u);
 #ifdef MPCD_TIMING
-    if (lane == 0) atomicAdd(&g_phase_cycles[8], (unsigned long long)(clock64() - tw0));
-    if (lane == 0) atomicAdd(&g_phase_cycles[9], 1ull);
+    if (lane == 0) S.tim[warp][8] += (unsigned long long)(clock64() - tw0);
+    if (lane == 0) S.tim[warp][9] += 1ull;
 #endif
     const int64_t c0 = tile * kTC;
     const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)kCW, A.C - c0 - cw0));
@@ -917,6 +927,9 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     }
     if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
   }
+#ifdef MPCD_TIMING
+  if (lane < 10) atomicAdd(&g_phase_cycles[lane], S.tim[warp][lane]);
+#endif
   // fused migration: this thread's stores into peers' regions become visible
   // system-wide before the step fence (the all-reduce that follows the step)
   if (A.peers) __threadfence_system();
