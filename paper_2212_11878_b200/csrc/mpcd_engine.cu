@@ -5,19 +5,23 @@
 // counts of both, and the overflow lists.  One step (engine.py:415-455 for
 // the whole box) is
 //
-//   k_step         every tile of 32 cells: gather the cells' records, rank by
-//                  id inside each cell (the reference's stable argsort over id
-//                  order), reduce (m v, m) in numpy's reduceat association,
-//                  com = p / m, the keyed Marsaglia axis, Rodrigues rotation,
-//                  stream + wrap, next-step cell; write the particle into
-//                  that cell's region (slot from an atomic on its count);
-//                  conservation / drift partials per tile.
-//   k_step_dense   the rare tiles with a full cell (overflow) or > 768 rows.
-//   k_diag_*       fixed-order reduction of the tile partials.
+//   k_step         persistent, warp-specialised: a producer warp stages each
+//                  16-cell tile with TMA bulk copies and draws its keyed
+//                  Marsaglia axes; each of 4 consumer warps takes 4 cells:
+//                  rank by id inside each cell (the reference's stable
+//                  argsort over id order), reduce (m v, m) in numpy's
+//                  reduceat association, com = p / m, Rodrigues rotation,
+//                  stream + wrap, next-step cell; the particle is written into
+//                  that cell's region (slot from an atomic on its count) --
+//                  or, in a decomposed box, into another rank's send buffer
+//                  or (fused migration) straight into that rank's region;
+//                  conservation / drift partials per CTA.
+//   k_step_dense   the rare tiles with a full cell (overflow) or too many rows.
+//   k_diag_*       fixed-order reduction of the CTA partials.
 //
 // Algorithmic bytes per particle-step: read 64 + write 64 (records) and, per
-// cell, read + zero its count (8) and one atomic on the next count (~8, L2).
-// See DESIGN.md section 3.
+// cell, read + zero its count and one atomic on the next count.  See
+// DESIGN.md section 3.
 #include <string.h>
 
 #include <algorithm>

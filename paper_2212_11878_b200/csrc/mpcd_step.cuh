@@ -185,9 +185,7 @@ __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c)
 #define MPCD_MINB 4
 #endif
 constexpr int kTC = MPCD_TC;    // cells per tile (one producer lane per cell, <= 32)
-constexpr int kNT = 256;        // threads of the step CTA
-constexpr int kPPT = 3;         // staged particles per thread
-constexpr int kMaxP = kNT * kPPT;  // padded staging slots per tile
+constexpr int kNT = 256;        // threads of the dense-tile CTA
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr int kDiagCols = 7;  // partial columns: px py pz sum(m v^2) mass collided migrated
 
@@ -949,7 +947,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 }
 
 // ----------------------------------------------------- dense-tile kernel --
-// Tiles with a cell above `cap` or more than kMaxP padded rows.  Gathers each
+// Tiles with a cell above `cap` or more than kMaxPT padded rows.  Gathers each
 // cell's region slots plus its overflow entries into HBM staging, then the
 // same phases with plain loops; ranking is O(k^2) per cell.  One CTA per
 // queued tile (grid-strided); staging ranges come from a bump allocator.
