@@ -135,3 +135,22 @@ def test_cuda_backend_needs_gpu_loudly():
         mp.Simulation(mp.SimParams(edge_length=4), backend="cuda")
     with pytest.raises(mp.ConfigError):
         mp.Simulation(mp.SimParams(edge_length=4), backend="threads")
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the oracle on the host cores) prints the
+    contract's JSON line without a GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "1", "--cpu-sample-L", "8"],
+                         capture_output=True, text=True, timeout=300, check=True).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["metric"] == "MPCD particle-steps/sec" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
