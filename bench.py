@@ -247,6 +247,8 @@ def run_ours(args):
         exch = DistExchange()
         fused = args.migration == "fused" and connect_fused(dom, exch)
         dom.init_device(params.n_particles, 1.0)
+        if fused:  # every rank's init precedes any rank's first step
+            exch.fence()
         ctx = dom.ctx
         runner_md = _DomainRunner(params, [dom], exch, capture_drift=False, capture_com=False,
                                   fused=fused)

@@ -485,6 +485,8 @@ class NcclRunner(_DomainRunner):
             domains = [domain_factory(params, layout, rank)]
             fused = False
         _initialise(domains, params, velocity_variance, init)
+        if fused:  # every rank's init (counts zeroed) precedes any rank's first step
+            exchange.fence()
         super().__init__(params, domains, exchange, capture_drift=capture_drift,
                          capture_com=capture_com, fused=fused)
         self.layout = layout
