@@ -179,3 +179,39 @@ def test_equivalence_check_serial_vs_decomposed_is_exact(scheme):
     assert rep.max_position_dev == 0.0
     assert rep.max_velocity_dev == 0.0
     assert rep.max_com_dev == 0.0
+
+
+@pytest.mark.parametrize("migration", ["fused", "exchange"])
+def test_dense_cluster_across_domain_boundary(migration):
+    """Clustered particles straddling a slab boundary: cells far above their
+    capacity (overflow lists, k_step_dense) on both sides, and -- fused --
+    overflow appends into the other domain's lists.  Must equal the whole box
+    and the oracle."""
+    import oracle
+
+    rs = np.random.default_rng(12)
+    n = 8000
+    pos = np.concatenate([rs.uniform([7.4, 3.1, 3.1], [8.6, 3.9, 3.9], size=(6000, 3)),
+                          rs.uniform(0, 16, size=(2000, 3))])
+    vel = rs.normal(size=(n, 3)) * 3.0
+    p = mp.ParticleSet(pos, vel, np.ones(n))
+    base = mp.SimParams(edge_length=16, seed=5, mean_density=n / 4096)
+    dec = mp.SimParams(edge_length=16, seed=5, mean_density=n / 4096, rank_dims=(2, 1, 1))
+    with mp.Simulation(base, backend="cuda") as whole, \
+            mp.Simulation(dec, backend="sequential", migration=migration) as parts:
+        whole.runner.ctx.upload(p.positions, p.velocities, None, None, 0)
+        for d in parts.runner.domains:
+            d.upload(p)
+        cs, sn = float(np.cos(base.alpha)), float(np.sin(base.alpha))
+        ref_pos, ref_vel = pos, vel
+        for k in range(4):
+            whole.step()
+            parts.step()
+            r = oracle.serial_step(ref_pos, ref_vel, np.ones(n), 16, 1.0, base.dt, cs, sn,
+                                   base.seed, k)
+            ref_pos, ref_vel = r.positions, r.velocities
+            (ia, pa), (ib, pb) = whole.collect(), parts.collect()
+            assert np.array_equal(pa.positions, ref_pos) and np.array_equal(pa.velocities, ref_vel)
+            assert np.array_equal(ia, ib)
+            assert np.array_equal(pa.positions, pb.positions), k
+            assert np.array_equal(pa.velocities, pb.velocities), k
