@@ -62,7 +62,10 @@ def parse():
     ap.add_argument("--L", type=int, default=256, help="cells per box edge (per GPU)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-sample-L", type=int, default=64)
+    ap.add_argument("--cpu-sample-L", type=int, default=128,
+                    help="cells per edge of the CPU (oracle) sample box")
+    ap.add_argument("--cpu-sample-steps", type=int, default=15,
+                    help="timed oracle steps of the cpu_baseline sample (~10 s of host work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--migration", default="fused", choices=("fused", "exchange"),
@@ -354,7 +357,7 @@ def run_ours(args):
     elif ws > 1 and not args.no_e2e:
         line["e2e"] = e2e_decomposed(args, params, dom, exch, fused)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args.cpu_sample_L, 3, args.seed)
+        line["cpu_baseline"] = cpu_baseline(args.cpu_sample_L, args.cpu_sample_steps, args.seed)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
