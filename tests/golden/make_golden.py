@@ -19,6 +19,10 @@ config1_L16.npz   BASELINE config 1 (16^3, 10/cell, 130 deg, seed 42):
                 initial state + per-step SHA-256 of the reference state,
                 cells, counts, permutation for 100 steps, diagnostics
 config2_L64.npz   64^3 seed 0: hash of the initial state and of 3 steps
+parallel_L8.npz   the reference's own rank-parallel step (backend
+                "sequential": halo scheme on (2,2,1), migration scheme on
+                (2,1,1)), per-step state and com capture, and the serial run
+                of the same config
 """
 
 from __future__ import annotations
@@ -242,6 +246,37 @@ def make_config2(steps=3):
     np.savez_compressed(os.path.join(HERE, "config2_L64.npz"), **out)
 
 
+def make_parallel(steps=5):
+    """The reference's multi-rank path (engine.py:190-391 through
+    runners.SequentialRunner) and its serial run, for the decomposed-box
+    parity tests (its own bound vs serial: 1e-10, test_engine.py:119-126)."""
+    out = {}
+    cases = {"halo": ((2, 2, 1), "halo"), "migr": ((2, 1, 1), "migration")}
+    for tag, (rank_dims, scheme) in cases.items():
+        params = SimParams(edge_length=8, seed=3, rank_dims=rank_dims, scheme=scheme)
+        sim = engine.Simulation(params, backend="sequential", capture_com=True)
+        for k in range(steps):
+            sim.step()
+            ids, p = sim.collect()
+            out[f"{tag}_ids{k}"] = ids
+            out[f"{tag}_pos{k}"] = p.positions
+            out[f"{tag}_vel{k}"] = p.velocities
+            ci, cv = sim.com_captures[-1]
+            out[f"{tag}_comids{k}"] = ci
+            out[f"{tag}_com{k}"] = cv
+        sim.close()
+        out[f"{tag}_rank_dims"] = np.array(rank_dims)
+    params = SimParams(edge_length=8, seed=3)
+    sim = engine.Simulation(params, backend="serial", capture_com=True)
+    for k in range(steps):
+        sim.step()
+        ids, p = sim.collect()
+        out[f"serial_pos{k}"] = p.positions
+        out[f"serial_vel{k}"] = p.velocities
+    out["steps"] = np.array(steps)
+    np.savez_compressed(os.path.join(HERE, "parallel_L8.npz"), **out)
+
+
 if __name__ == "__main__":
     print("numpy", np.__version__, "reference", REF_SRC)
     make_rng()
@@ -249,6 +284,7 @@ if __name__ == "__main__":
     make_serial_small()
     make_config1()
     make_config2()
+    make_parallel()
     with open(os.path.join(HERE, "PROVENANCE.txt"), "w") as f:
         f.write(f"generated by tests/golden/make_golden.py from {REF_SRC}\n")
         f.write(f"numpy {np.__version__}, python {sys.version.split()[0]}\n")

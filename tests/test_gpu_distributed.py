@@ -215,3 +215,32 @@ def test_dense_cluster_across_domain_boundary(migration):
             assert np.array_equal(ia, ib)
             assert np.array_equal(pa.positions, pb.positions), k
             assert np.array_equal(pa.velocities, pb.velocities), k
+
+
+@pytest.mark.parametrize("tag", ["halo", "migr"])
+@pytest.mark.parametrize("migration", ["fused", "exchange"])
+def test_matches_reference_parallel_runs(tag, migration):
+    """Against the reference's OWN rank-parallel step (golden parallel_L8.npz,
+    its "sequential" runner, halo scheme on (2,2,1) and migration scheme on
+    (2,1,1)): within the reference's bound of 1e-10 (test_engine.py:119-126),
+    and bitwise equal to the reference's serial run of the same config."""
+    from conftest import golden
+
+    g = golden("parallel_L8.npz")
+    rank_dims = tuple(int(x) for x in g[f"{tag}_rank_dims"])
+    params = mp.SimParams(edge_length=8, seed=3, rank_dims=rank_dims,
+                          scheme="halo" if tag == "halo" else "migration")
+    with mp.Simulation(params, backend="sequential", capture_com=True,
+                       migration=migration) as sim:
+        for k in range(int(g["steps"])):
+            sim.step()
+            ids, p = sim.collect()
+            assert np.array_equal(ids, g[f"{tag}_ids{k}"])
+            d = np.abs(p.positions - g[f"{tag}_pos{k}"])
+            assert np.minimum(d, 8.0 - d).max() <= 1e-10
+            assert np.abs(p.velocities - g[f"{tag}_vel{k}"]).max() <= 1e-10
+            assert np.array_equal(p.positions, g[f"serial_pos{k}"])
+            assert np.array_equal(p.velocities, g[f"serial_vel{k}"])
+            ci, cv = sim.com_captures[-1]
+            assert np.array_equal(ci, g[f"{tag}_comids{k}"])
+            assert np.abs(cv - g[f"{tag}_com{k}"]).max() <= 1e-10
