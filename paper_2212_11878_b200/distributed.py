@@ -108,6 +108,10 @@ def default_send_capacity(layout: DomainLayout, mean_density: float) -> int:
 
 # --------------------------------------------------------------- exchange --
 def _check_overflow(counts: np.ndarray, cap: int):
+    """Every rank checks the same all-gathered matrix, so all raise together."""
+    if counts.size and np.any(np.diag(counts)):
+        r = int(np.argmax(np.diag(counts)))
+        raise TopologyError(f"rank {r} routed particles to itself")
     if counts.size and int(counts.max()) > cap:
         src, dst = np.unravel_index(int(np.argmax(counts)), counts.shape)
         raise MpcdError(f"migration buffer overflow: rank {src} sends {int(counts.max())} "
@@ -202,8 +206,6 @@ class DistExchange:
             if c and peer != me:
                 ops.append(dist.P2POp(dist.isend, self._stage(dom.send_view(peer, c)), peer,
                                       group=self.group))
-        if int(counts[me, me]):
-            raise TopologyError(f"rank {me} routed particles to itself")
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
