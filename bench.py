@@ -349,7 +349,8 @@ def run_ours(args):
             "b_min_frac": B_MIN_N * n / (ms * 1e-3) / 1e9 / peak,
             "kernel_ms": per_kernel},
         "gpu_launches": args.steps * (LAUNCHES_PER_STEP + (1 if ws > 1 and not fused else 0)),
-        "diag_last": {"momentum": list(d.momentum), "energy": d.energy, "mass": d.mass},
+        "diag_last": {"momentum": list(d.momentum), "energy": d.energy, "mass": d.mass,
+                      "collided": int(d.n), "migrated": int(d.migrated)},
     }
     line["clocks"] = clocks.summary()
     if ws == 1 and not args.no_e2e:
