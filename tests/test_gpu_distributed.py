@@ -244,3 +244,17 @@ def test_matches_reference_parallel_runs(tag, migration):
             ci, cv = sim.com_captures[-1]
             assert np.array_equal(ci, g[f"{tag}_comids{k}"])
             assert np.abs(cv - g[f"{tag}_com{k}"]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("migration", ["fused", "exchange"])
+def test_non_unit_cell_size_and_prng_domains(migration):
+    """cell_size != 1 (IEEE division in the binning), a short dt, a 3 x 1 x 2
+    rank grid and the pcg32 generator: still the whole box bit for bit."""
+    kw = dict(edge_length=12, cell_size=0.5, dt=0.05, seed=21, prng="pcg32")
+    ids_a, pa, _, ca, _ = run(mp.SimParams(**kw), "cuda", 5, capture_com=True)
+    ids_b, pb, _, cb, _ = run(mp.SimParams(rank_dims=(3, 1, 2), **kw), "sequential", 5,
+                              capture_com=True, migration=migration)
+    assert np.array_equal(ids_a, ids_b)
+    assert np.array_equal(pa.positions, pb.positions)
+    assert np.array_equal(pa.velocities, pb.velocities)
+    assert np.array_equal(ca[-1][0], cb[-1][0]) and np.array_equal(ca[-1][1], cb[-1][1])
