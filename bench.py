@@ -68,6 +68,9 @@ def parse():
                     help="timed oracle steps of the cpu_baseline sample (~10 s of host work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", type=int, default=4, choices=(4, 5),
+                    help="N > 1: 4 = (256 N) x 256 x 256 slabs (weak), 5 = 1024 x 512 x 512 "
+                         "pencils (strong, 8 GPUs)")
     ap.add_argument("--migration", default="fused", choices=("fused", "exchange"),
                     help="N > 1: particle migration inside k_step over peer memory, or "
                          "through send buffers + NCCL point-to-point")
@@ -242,9 +245,17 @@ def run_ours(args):
         # peer memory cannot be opened).
         from paper_2212_11878_b200.distributed import (CudaDomain, DistExchange, DomainLayout,
                                                        _DomainRunner, connect_fused)
-        dims = (L * ws, L, L)
+        if args.config == 5:
+            # BASELINE config 5: 1024 x 512 x 512 cells (2.7 G particles) strong
+            # scaling, pencil decomposition (8 GPUs: 4 x 2 x 1)
+            dims = (1024, 512, 512)
+            rank_dims = {8: (4, 2, 1), 16: (4, 2, 2)}.get(ws)
+            if rank_dims is None:
+                raise SystemExit("config 5 needs 8 GPUs (1.1 TB of cell regions)")
+        else:
+            dims, rank_dims = (L * ws, L, L), (ws, 1, 1)
         params = SimParams(edge_length=dims[0], edge_lengths=dims, seed=args.seed,
-                           rank_dims=(ws, 1, 1))
+                           rank_dims=rank_dims)
         layout = DomainLayout.from_params(params)
         dom = CudaDomain(params, layout, rank)
         exch = DistExchange()
@@ -261,7 +272,7 @@ def run_ours(args):
         def run_steps(first, count):
             for k in range(first, first + count):
                 runner_md.advance(k, 0)
-    C = L ** 3
+    C = L ** 3 if ws == 1 else int(np.prod(layout.local_dims))  # cells per GPU
     run_steps(0, args.warmup)
     torch.cuda.synchronize()
 
@@ -318,19 +329,21 @@ def run_ours(args):
     survey_bytes = SURVEY_B_ALG_N * n + SURVEY_B_ALG_C * C
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 and args.config == 5 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (device init_system: uniform positions, N(0,1) velocities minus "
                 "their mean, unit masses)",
-        "config": {"workload": f"{L}^3 cells x 10 particles/cell periodic SRD box per GPU "
-                               f"(BASELINE config {'3' if L == 256 else 'custom'}), 130 deg, "
-                               "dt 0.1, splitmix keyed RNG",
+        "config": {"workload": workload_text(args, ws, params),
                    "cells_per_gpu": C, "particles_per_gpu": n,
                    "parallelism": "single domain" if ws == 1 else
-                   f"slab decomposition ({ws},1,1) of a {L * ws}x{L}x{L} box (BASELINE "
-                   "config 4), particle migration every step: " +
-                   ("fused into k_step over NVLink peer memory, NCCL all-reduce step fence"
-                    if ws > 1 and fused else "send buffers + NCCL point-to-point"),
+                   f"{'slab' if params.rank_dims[1:] == (1, 1) else 'pencil'} decomposition "
+                   f"{tuple(params.rank_dims)} of a {'x'.join(map(str, params.dims))} box, "
+                   "particle migration every step: " +
+                   ("fused into k_step over peer memory, " +
+                    ("gloo barrier step fence (host-staged check mode)" if exch.host_staged
+                     else "NCCL all-reduce step fence")
+                    if fused else "send buffers + point-to-point exchange"),
                    "l2": "state 17 GB >> 126 MB L2; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -364,6 +377,19 @@ def run_ours(args):
     ctx.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def workload_text(args, ws, params):
+    dims = "x".join(map(str, params.dims))
+    if ws == 1:
+        which = "BASELINE config 3" if args.L == 256 else "custom size"
+        return (f"{dims} cells x 10 particles/cell periodic SRD box ({which}), 130 deg, dt 0.1, "
+                "splitmix keyed RNG")
+    if args.config == 5:
+        return (f"{dims} cells x 10 particles/cell (BASELINE config 5, strong scaling over "
+                f"{ws} GPUs), 130 deg, dt 0.1, splitmix keyed RNG")
+    return (f"{args.L}^3 cells x 10 particles/cell per GPU, {dims} box (BASELINE config 4, weak "
+            "scaling), 130 deg, dt 0.1, splitmix keyed RNG")
 
 
 def e2e_decomposed(args, params, dom, exch, fused):
