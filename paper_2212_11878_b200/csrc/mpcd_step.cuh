@@ -95,11 +95,26 @@ __device__ __forceinline__ void count_zero(uint32_t* p) {
                : "memory");
 }
 
+// One 32-byte record with a single 256-bit store (sm_100: STG.256), streaming.
+#ifndef MPCD_ST256
+#define MPCD_ST256 1
+#endif
+__device__ __forceinline__ void st4(void* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ void store_rec(const Recs& s, uint64_t dst, double x, double y,
                                           double z, uint32_t id, double vx, double vy, double vz,
                                           double m) {
   PRec* pr = s.p + dst;
   VRec* vr = s.v + dst;
+  if (MPCD_ST256) {
+    st4(pr, x, y, z, id_bits(id));
+    st4(vr, vx, vy, vz, m);
+    return;
+  }
   st2(&pr->x, x, y);
   st2(&pr->z, z, id_bits(id));
   st2(&vr->vx, vx, vy);
