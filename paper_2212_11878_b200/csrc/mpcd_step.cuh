@@ -202,6 +202,7 @@ __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c)
 constexpr int kTC = MPCD_TC;    // cells per tile (one producer lane per cell, <= 32)
 constexpr int kNT = 256;        // threads of the dense-tile CTA
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+constexpr int kPadBit = 0x80;  // slot-table flag of a padding slot
 constexpr int kDiagCols = 7;  // partial columns: px py pz sum(m v^2) mass collided migrated
 
 // ------------------------------------------------------------ cell index --
@@ -542,7 +543,7 @@ static_assert(kTC % kCW == 0 && kTC <= 32, "tile = whole consumer warps, one pro
 struct TileBuf {
   PRec p[kMaxPT];
   VRec v[kMaxPT];
-  double ax[kTC * 3];
+  double ax[kTC * 4];  // axis of each cell, padded to 4 doubles (two 16-byte loads)
   uint32_t cnt[kTC];
   uint32_t off[kTC + 1];
   uint8_t cell[kMaxPT];
@@ -556,7 +557,7 @@ struct __align__(16) WarpScratch {
   double val[(kSlotsW + kCW) * 4];  // (m v, m) rows in rank order; post rows later
   uint32_t id[kSlotsW];             // ids in slot order, sentinel in padding
   double mom[kCW * 4];
-  double com[kCW * 3];
+  double com[kCW * 4];  // com of each cell, padded to 4 doubles
 };
 
 #ifndef MPCD_STAGES
@@ -661,10 +662,11 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
     asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(q));
   }
 #endif
-  for (uint32_t j = excl; j < incl; ++j) B.cell[j] = (uint8_t)lane;
+  // slot -> cell, bit 7 set on a padding slot
+  for (uint32_t j = excl; j < incl; ++j) B.cell[j] = (uint8_t)(lane | (j - excl < k ? 0 : kPadBit));
   // rotation axes (collision.py:217-250), keyed by the global cell id
   if (lane < kTC) {
-    double* ax = B.ax + lane * 3;
+    double* ax = B.ax + lane * 4;
     ax[0] = ax[1] = ax[2] = 0.0;
     if (cnt > 0u && !rotation_axis_pre(A.prng, A.axis_prefix, global_cell_id<MODE>(A, c0 + lane), ax))
       atomicOr(&A.flags[1], 1u);
@@ -694,9 +696,9 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     real[r] = false;
     lq[r] = 0;
     if (j < j1) {
-      const int lc = T.cell[j];
-      lq[r] = lc - cw0;
-      real[r] = (uint32_t)j - T.off[lc] < T.cnt[lc];
+      const int cj = T.cell[j];
+      lq[r] = (cj & ~kPadBit) - cw0;
+      real[r] = !(cj & kPadBit);
       W.id[jl] = real[r] ? T.p[j].id : kSentinel;
     }
   }
@@ -747,7 +749,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       W.mom[lane] = mom;
       const double c = (comp < 3) ? ((mass > 0.0) ? mom / mass : 0.0)
                                   : (double)T.cnt[cw0 + q];
-      if (comp < 3) W.com[q * 3 + comp] = c;
+      if (comp < 3) W.com[q * 4 + comp] = c;
       else {
         acc[4] += mass;
         acc[5] += (double)T.cnt[cw0 + q];  // particles collided
@@ -776,8 +778,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       double2 p01, p23, v01, v23;  // x y | z id, vx vy | vz m
       lds_row32(T.p, j, p01, p23);
       lds_row32(T.v, j, v01, v23);
-      const double* cx = W.com + lq[r] * 3;
-      const double* ax = T.ax + (cw0 + lq[r]) * 3;
+      double2 c01, c2, a01, a2;
+      lds_row32(W.com + lq[r] * 4, 0, c01, c2);
+      lds_row32(T.ax + (cw0 + lq[r]) * 4, 0, a01, a2);
+      const double cx[3] = {c01.x, c01.y, c2.x}, ax[3] = {a01.x, a01.y, a2.x};
       double v[3] = {v01.x, v01.y, v23.x}, w[3];
       rotate(v, cx, ax, A.cs, A.sn, w);
       o[r][0] = wrap_fast(p01.x + w[0] * A.dt, A.box0);
