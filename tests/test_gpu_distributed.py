@@ -82,7 +82,7 @@ def test_one_domain_nccl_equals_cuda():
     assert all(d["crossings"] == 0 for d in db)
 
 
-@pytest.mark.parametrize("prng", ["splitmix", "pcg32"])
+@pytest.mark.parametrize("prng", ["splitmix", "pcg32", "minstd", "sfc64"])
 def test_device_init_domains_equal_whole_box(prng):
     dims = (32, 32, 32)
     base = mp.SimParams(edge_length=32, seed=7, prng=prng)
@@ -258,3 +258,17 @@ def test_non_unit_cell_size_and_prng_domains(migration):
     assert np.array_equal(pa.positions, pb.positions)
     assert np.array_equal(pa.velocities, pb.velocities)
     assert np.array_equal(ca[-1][0], cb[-1][0]) and np.array_equal(ca[-1][1], cb[-1][1])
+
+
+@pytest.mark.parametrize("prng", ["splitmix", "minstd", "pcg32", "sfc64"])
+def test_config2_64cubed_domains_equal_whole_box(prng):
+    """BASELINE config 2 (64^3 x 10 = 2.6 M particles) on a 2 x 2 x 2 domain
+    grid with fused migration, every PRNG: the whole box bit for bit."""
+    base = mp.SimParams(edge_length=64, seed=0, prng=prng)
+    dec = mp.SimParams(edge_length=64, seed=0, prng=prng, rank_dims=(2, 2, 2))
+    ids_a, pa, da, _, _ = run(base, "cuda", 3, init="device")
+    ids_b, pb, db, _, _ = run(dec, "sequential", 3, init="device")
+    assert np.array_equal(ids_a, ids_b)
+    assert np.array_equal(pa.positions, pb.positions)
+    assert np.array_equal(pa.velocities, pb.velocities)
+    assert all(d["crossings"] > 0 for d in db)
