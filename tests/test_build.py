@@ -86,3 +86,7 @@ def test_sass_has_tma_and_mbarrier():
                           text=True).stdout
     assert "UBLKCP" in sass
     assert "SYNCS" in sass
+    # one 256-bit store per 32-byte particle record (sm_100 STG.256)
+    assert re.search(r"STG\.E\.[A-Z0-9.]*256", sass)
+    # the fused migration's system-scope fence
+    assert "MEMBAR" in sass
