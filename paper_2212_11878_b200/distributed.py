@@ -358,6 +358,7 @@ class _DomainRunner:
                  for d in self.domains]
         parts = sorted((x for g in self._gather(local) for x in g), key=lambda x: x[0])
         diag = _merge([p[1] for p in parts], int(sum(p[1][8] for p in parts)))
+        diag["sending_domains"] = int(sum(1 for p in parts if p[1][8] > 0))
         if self.capture_drift:
             diag["max_cell_drift"] = max(float(p[1][5]) for p in parts)
         if self.capture_com:

@@ -272,3 +272,30 @@ def test_config2_64cubed_domains_equal_whole_box(prng):
     assert np.array_equal(pa.positions, pb.positions)
     assert np.array_equal(pa.velocities, pb.velocities)
     assert all(d["crossings"] > 0 for d in db)
+
+
+def test_benchmark_report_cases_and_matrix(tmp_path):
+    """mpcdsim.bench on the GPU backends (the reference's test_bench_cli.py:43-104)."""
+    from paper_2212_11878_b200 import bench
+
+    params = mp.SimParams(edge_length=8, mean_density=4.0, rank_dims=(2, 1, 1), n_steps=3)
+    rec = bench.run_benchmark_case(params, steps=3, warmup=1)
+    assert rec.L == 8 and rec.ranks == 2 and rec.steps == 3
+    assert rec.particles == params.n_particles and rec.seconds > 0.0
+    assert rec.bytes_per_step > 0.0 and rec.msgs_per_step > 0.0
+    assert rec.max_drift < 1e-11 and rec.error == ""
+    one = bench.run_benchmark_case(mp.SimParams(edge_length=8, mean_density=4.0), steps=2,
+                                   warmup=1)
+    assert one.ranks == 1 and one.bytes_per_step == 0.0
+    with pytest.raises(mp.ConfigError):
+        bench.run_benchmark_case(params, steps=0, warmup=1)
+    seen = []
+    recs = bench.run_benchmark_matrix(sizes=(8,), rank_counts=(1, 2, 3), steps=2, warmup=1,
+                                      density=4.0,
+                                      progress=lambda L, s, r: seen.append((L, s, r)))
+    assert seen == [(8, "halo", 1), (8, "halo", 2), (8, "halo", 3)]
+    assert recs[0].error == "" and recs[1].error == ""
+    assert "ConfigError" in recs[2].error and recs[2].seconds == 0.0
+    path = tmp_path / "b.csv"
+    bench.emit_report(recs, str(path))
+    assert bench.read_report(str(path)) == recs
