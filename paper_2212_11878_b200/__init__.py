@@ -29,9 +29,20 @@ from .collision import (
     sample_rotation_axis,
     segment_moments,
 )
+from .decomposition import (
+    CODE_STAY,
+    DomainGrid,
+    build_decomposition,
+    classify_base3,
+    code_digits,
+    neighbor_rank,
+    reflect_code,
+)
 from .engine import (
     BACKEND_CUDA,
     BACKEND_NCCL,
+    BACKEND_PROCESS,
+    BACKEND_SEQUENTIAL,
     BACKEND_SERIAL,
     POLICY_IMMEDIATE,
     POLICY_LAZY,

@@ -31,7 +31,10 @@ BACKEND_CUDA = "cuda"
 BACKEND_NCCL = "nccl"
 BACKEND_SERIAL = "serial"  # alias of "cuda" (the single-domain path)
 BACKEND_SEQUENTIAL = "sequential"  # decomposed box, every domain in this process
-BACKENDS = (BACKEND_CUDA, BACKEND_NCCL, BACKEND_SERIAL, BACKEND_SEQUENTIAL)
+# the reference's one-worker-process-per-rank backend: here the same domains
+# run in this process on this GPU ("nccl" is the one-process-per-GPU form)
+BACKEND_PROCESS = "process"
+BACKENDS = (BACKEND_CUDA, BACKEND_NCCL, BACKEND_SERIAL, BACKEND_SEQUENTIAL, BACKEND_PROCESS)
 POLICY_IMMEDIATE = "immediate"
 POLICY_LAZY = "lazy"
 POLICIES = (POLICY_IMMEDIATE, POLICY_LAZY)
@@ -345,7 +348,7 @@ class Simulation:
             self._runner = CudaRunner(params, capture_drift=capture_drift,
                                       capture_com=capture_com,
                                       velocity_variance=velocity_variance, init=init)
-        elif backend in (BACKEND_NCCL, BACKEND_SEQUENTIAL):
+        elif backend in (BACKEND_NCCL, BACKEND_SEQUENTIAL, BACKEND_PROCESS):
             from .distributed import NcclRunner, SequentialRunner
             cls = NcclRunner if backend == BACKEND_NCCL else SequentialRunner
             self._runner = cls(params, policy=policy, capture_drift=capture_drift,

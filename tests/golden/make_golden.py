@@ -19,6 +19,8 @@ config1_L16.npz   BASELINE config 1 (16^3, 10/cell, 130 deg, seed 42):
                 initial state + per-step SHA-256 of the reference state,
                 cells, counts, permutation for 100 steps, diagnostics
 config2_L64.npz   64^3 seed 0: hash of the initial state and of 3 steps
+decomposition.npz rank grids (neighbour tables, borders, coordinates),
+                base-3 side codes of random and border positions
 parallel_L8.npz   the reference's own rank-parallel step (backend
                 "sequential": halo scheme on (2,2,1), migration scheme on
                 (2,1,1)), per-step state and com capture, and the serial run
@@ -277,6 +279,32 @@ def make_parallel(steps=5):
     np.savez_compressed(os.path.join(HERE, "parallel_L8.npz"), **out)
 
 
+def make_decomposition():
+    from mpcdsim import decomposition as dec
+
+    out = {}
+    rs = np.random.default_rng(99)
+    cases = [(8, 1.0, (2, 2, 2)), (12, 0.5, (3, 2, 1)), (6, 2.0, (1, 3, 2)), (4, 1.0, (1, 1, 1))]
+    for i, (L, a, rd) in enumerate(cases):
+        g = dec.build_decomposition(L, a, rd)
+        out[f"c{i}_own"] = g.own_cells
+        out[f"c{i}_table"] = g.neighbor_table
+        out[f"c{i}_borders"] = np.array([g.dom_borders(r) for r in range(g.n_ranks)])
+        out[f"c{i}_coords"] = np.array([g.rank_coords(r) for r in range(g.n_ranks)])
+        gc = rs.integers(-2 * L, 3 * L, size=(50, 3))
+        out[f"c{i}_gc"] = gc
+        out[f"c{i}_flat"] = g.global_flat_cells(gc)
+        box = L * a
+        pos = rs.uniform(-0.2 * box, 1.2 * box, size=(400, 3))
+        pos[:40] = np.round(pos[:40] / (a * g.own_cells)) * (a * g.own_cells)  # on borders
+        out[f"c{i}_pos"] = pos
+        out[f"c{i}_codes"] = np.array([dec.classify_base3(pos, g.dom_borders(r))
+                                       for r in range(g.n_ranks)])
+    out["digits"] = dec.code_digits(np.arange(27))
+    out["reflect"] = np.array([dec.reflect_code(c) for c in range(27)])
+    np.savez_compressed(os.path.join(HERE, "decomposition.npz"), **out)
+
+
 if __name__ == "__main__":
     print("numpy", np.__version__, "reference", REF_SRC)
     make_rng()
@@ -285,6 +313,7 @@ if __name__ == "__main__":
     make_config1()
     make_config2()
     make_parallel()
+    make_decomposition()
     with open(os.path.join(HERE, "PROVENANCE.txt"), "w") as f:
         f.write(f"generated by tests/golden/make_golden.py from {REF_SRC}\n")
         f.write(f"numpy {np.__version__}, python {sys.version.split()[0]}\n")
