@@ -299,3 +299,13 @@ def test_benchmark_report_cases_and_matrix(tmp_path):
     path = tmp_path / "b.csv"
     bench.emit_report(recs, str(path))
     assert bench.read_report(str(path)) == recs
+
+
+def test_process_backend_alias_runs_the_domains_in_process():
+    """The reference's "process" backend name (one worker per rank there)
+    runs the same decomposition in this process here."""
+    params = mp.SimParams(edge_length=8, seed=6, rank_dims=(2, 1, 1))
+    ids_a, pa, _, _, _ = run(mp.SimParams(edge_length=8, seed=6), "cuda", 3)
+    ids_b, pb, _, _, _ = run(params, mp.BACKEND_PROCESS, 3)
+    assert np.array_equal(pa.positions, pb.positions)
+    assert np.array_equal(pa.velocities, pb.velocities)
