@@ -681,7 +681,7 @@ int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_
   return kDenseGrid;
 }
 
-// 48 compile-time variants, chosen at run time
+// 64 compile-time variants, chosen at run time
 struct Variant {
   bool unit, umass, drift, com;
   int mode;
@@ -690,6 +690,7 @@ template <bool UNIT, bool UMASS, bool DRIFT, bool COM>
 int64_t launch_mode(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
   if (v.mode == kById) return launch_variant<UNIT, UMASS, DRIFT, COM, kById>(A, nt, which, st);
   if (v.mode == kMulti) return launch_variant<UNIT, UMASS, DRIFT, COM, kMulti>(A, nt, which, st);
+  if (v.mode == kFused) return launch_variant<UNIT, UMASS, DRIFT, COM, kFused>(A, nt, which, st);
   return launch_variant<UNIT, UMASS, DRIFT, COM, kBinned>(A, nt, which, st);
 }
 template <bool UNIT, bool UMASS, bool DRIFT>
@@ -731,7 +732,7 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
   }
   const Variant v{c->cfg.cell_size == 1.0, c->cfg.uniform_mass != 0,
                   (flags & MPCD_STEP_WANT_DRIFT) != 0, com,
-                  by_id ? kById : (c->multi ? kMulti : kBinned)};
+                  by_id ? kById : (c->multi ? (c->p2p ? kFused : kMulti) : kBinned)};
   const int64_t grid = launch_step_kernel(A, c->ntiles, v, 0, st);
   MPCD_LAUNCH_CHECK();
   if (ev) MPCD_CUDA(cudaEventRecord(ev[1], st));

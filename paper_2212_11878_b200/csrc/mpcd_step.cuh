@@ -16,8 +16,10 @@
 // unused), DRIFT (capture_drift: per-cell post-collision moments in numpy
 // order), COM (capture_com: com rows to HBM), MODE: kBinned (one domain),
 // kById (pure-function mode: write row `id` of a flat array, no next
-// binning) or kMulti (one domain of a decomposed box: leavers are written to
-// per-rank send buffers instead of a local cell).
+// binning), kMulti (one domain of a decomposed box: leavers are written to
+// per-rank send buffers instead of a local cell) or kFused (the same, leavers
+// written straight into their owner's cells over peer memory).  Each mode
+// compiles only its own leaver path, which keeps the hot loop's code small.
 #pragma once
 
 namespace mpcd {
@@ -177,15 +179,18 @@ struct StepArgs {
 };
 
 // Step kernel modes: binned single domain, by-id pure function, multi-domain
-constexpr int kBinned = 0, kById = 1, kMulti = 2;
+constexpr int kBinned = 0, kById = 1, kMulti = 2, kFused = 3;
+__host__ __device__ constexpr bool decomposed(int mode) { return mode >= kMulti; }
 
 // Global (whole-box) id of local cell c: the key of its rotation axis
 // (engine.py:82-92, 225-227 key axes by the global cell id).
 template <int MODE>
 __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c) {
-  if (MODE != kMulti) return (uint64_t)c;
-  const int64_t lz = c % A.L2, t = c / A.L2;
-  const int64_t ly = t % A.L1, lx = t / A.L1;
+  if (!decomposed(MODE)) return (uint64_t)c;
+  // 32-bit division: a context holds fewer than 2^32 cells (mpcd_ctx_create)
+  const uint32_t cc = (uint32_t)c, l2 = (uint32_t)A.L2, l1 = (uint32_t)A.L1;
+  const uint32_t t = cc / l2, lz = cc - t * l2;
+  const uint32_t lx = t / l1, ly = t - lx * l1;
   return ((uint64_t)(lx + A.o0) * (uint64_t)A.G1 + (uint64_t)(ly + A.o1)) * (uint64_t)A.G2 +
          (uint64_t)(lz + A.o2);
 }
@@ -374,10 +379,11 @@ __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, uns
 // Multi-domain leavers: one atomic per destination rank per warp; a
 // destination's count may run past send_cap (the host sees it and fails).
 // Must be reached by the whole warp.
+template <bool FUSED>
 __device__ __forceinline__ void send_foreign(const StepArgs& A, bool active, int dest,
                                              uint32_t key, const double* o, uint32_t id,
                                              double m, double& migrated) {
-  if (A.peers) {  // fused: claim a slot in the owner's next-step cell, store there
+  if (FUSED) {  // claim a slot in the owner's next-step cell, store there
     if (!active) return;
     migrated += 1.0;
     const PeerBufs& P = A.peers[dest];
@@ -427,10 +433,10 @@ __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, 
   }
   uint32_t key = 0u;
   bool local = active;
-  if (MODE == kMulti) {
+  if (decomposed(MODE)) {
     int dest = 0;
     if (active) local = next_cell_multi<UNIT>(A, nx, ny, nz, key, dest);
-    send_foreign(A, active && !local, dest, key, o, id, m, migrated);
+    send_foreign<MODE == kFused>(A, active && !local, dest, key, o, id, m, migrated);
   } else if (active) {
     key = next_cell<UNIT>(A, nx, ny, nz);
   }
@@ -790,7 +796,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
       pid[r] = bits_id(p23.y);
       mm[r] = UMASS ? A.m0 : v23.y;
-      if (MODE == kMulti)
+      if (decomposed(MODE))
         stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]);
       else
         key[r] = BYID ? pid[r] : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
@@ -813,8 +819,9 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       grp[r] = 0u;
       base[r] = 0u;
       if (j0 + 32 * r < j1) {  // warp-uniform: every lane takes part in the ballot
-        if (MODE == kMulti)
-          send_foreign(A, real[r] && !stay[r], dest[r], key[r], o[r], pid[r], mm[r], acc[6]);
+        if (decomposed(MODE))
+          send_foreign<MODE == kFused>(A, real[r] && !stay[r], dest[r], key[r], o[r], pid[r],
+                                       mm[r], acc[6]);
         claim_slot(A, stay[r], key[r], grp[r], base[r]);
       }
     }
