@@ -234,6 +234,47 @@ __device__ __forceinline__ uint32_t next_cell(const StepArgs& A, double x, doubl
   return (ix * (unsigned)A.L1 + iy) * (unsigned)A.L2 + iz;
 }
 
+// A leaver's owner and its cell in the owner's numbering (uniform blocks:
+// global mod block), packed (dest << 32 | key).  Out of line: the divisions
+// are rare and would otherwise bloat every inlined copy of the hot loop.
+__device__ __noinline__ uint64_t foreign_target(int gx, int gy, int gz, int L0, int L1, int L2,
+                                                int R1, int R2) {
+  const int dest = ((gx / L0) * R1 + gy / L1) * R2 + gz / L2;
+  const uint32_t key = ((uint32_t)(gx % L0) * (uint32_t)L1 + (uint32_t)(gy % L1)) * (uint32_t)L2 +
+                       (uint32_t)(gz % L2);
+  return ((uint64_t)(uint32_t)dest << 32) | key;
+}
+
+// Fused migration of one leaver: claim a slot in its owner's next-step cell
+// and store it there over peer memory (or the owner's overflow list).  Out
+// of line, scalar arguments only (no address of the kernel's parameters).
+__device__ __noinline__ void fused_put(const PeerBufs* peers, int b, uint32_t cap,
+                                       uint32_t ovf_cap, int dest, uint32_t key, double x,
+                                       double y, double z, uint32_t id, double vx, double vy,
+                                       double vz, double m) {
+  const PeerBufs& P = peers[dest];
+  const uint32_t slot = atomicAdd(&P.count[b][key], 1u);
+  // two 16-byte stores per record here: ptxas mis-assembles the 256-bit
+  // inline-asm store inside a called (non-inlined) function
+  auto put = [&](const Recs& r, uint64_t dst) {
+    st2(&r.p[dst].x, x, y);
+    st2(&r.p[dst].z, z, id_bits(id));
+    st2(&r.v[dst].vx, vx, vy);
+    st2(&r.v[dst].vz, vz, m);
+  };
+  if (slot < cap) {
+    put(P.reg[b], (uint64_t)key * cap + slot);
+  } else {  // the owner's cell is full: its overflow list
+    const uint32_t q = atomicAdd(&P.small[4 + b], 1u);
+    if (q < ovf_cap) {
+      put(P.ovf[b], q);
+      P.ovf_cell[b][q] = key;
+    } else {
+      atomicOr(&P.small[2], 1u);
+    }
+  }
+}
+
 // Multi-domain: the next-step cell in global coordinates (the serial
 // formula, so binning is bit-identical to one domain); true and the local
 // key when this domain owns it, else false and the owning rank.
@@ -248,10 +289,9 @@ __device__ __forceinline__ bool next_cell_multi(const StepArgs& A, double x, dou
     key = (lx * (unsigned)A.L1 + ly) * (unsigned)A.L2 + lz;
     return true;
   }
-  dest = ((gx / A.L0) * A.R1 + gy / A.L1) * A.R2 + gz / A.L2;
-  // the cell in the owner's numbering (uniform blocks: global mod block)
-  key = ((unsigned)(gx % A.L0) * (unsigned)A.L1 + (unsigned)(gy % A.L1)) * (unsigned)A.L2 +
-        (unsigned)(gz % A.L2);
+  const uint64_t t = foreign_target(gx, gy, gz, A.L0, A.L1, A.L2, A.R1, A.R2);
+  dest = (int)(t >> 32);
+  key = (uint32_t)t;
   return false;
 }
 
@@ -386,20 +426,8 @@ __device__ __forceinline__ void send_foreign(const StepArgs& A, bool active, int
   if (FUSED) {  // claim a slot in the owner's next-step cell, store there
     if (!active) return;
     migrated += 1.0;
-    const PeerBufs& P = A.peers[dest];
-    const int b = A.out_set;
-    const uint32_t slot = atomicAdd(&P.count[b][key], 1u);
-    if (slot < A.cap) {
-      store_rec(P.reg[b], (uint64_t)key * A.cap + slot, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
-    } else {  // the owner's cell is full: its overflow list
-      const uint32_t q = atomicAdd(&P.small[4 + b], 1u);
-      if (q < A.ovf_cap) {
-        store_rec(P.ovf[b], q, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
-        P.ovf_cell[b][q] = key;
-      } else {
-        atomicOr(&P.small[2], 1u);
-      }
-    }
+    fused_put(A.peers, A.out_set, A.cap, A.ovf_cap, dest, key, o[0], o[1], o[2], id, o[3], o[4],
+              o[5], m);
     return;
   }
   const unsigned act = __ballot_sync(0xffffffffu, active);
