@@ -800,8 +800,9 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   uint32_t key[R];
   double mm[R];
   uint32_t pid[R];
-  bool stay[R];  // kMulti: the next cell is this domain's
+  bool stay[R];  // decomposed: the next cell is this domain's
   int dest[R];
+  unsigned leavers = 0u;  // decomposed: bit r, row r's particle goes to another domain
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     key[r] = 0u;
@@ -831,6 +832,18 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       const double m = mm[r];
       sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]),
                 make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2])));
+      if (decomposed(MODE) && !stay[r]) {
+        // a leaver: park its record in its own tile slot (dest in the pad
+        // word) and its owner-local cell in W.id; flushed after the pass, so
+        // the hot loop carries no copy of the sending code
+        sts_row32(T.p, j, make_double2(o[r][0], o[r][1]),
+                  make_double2(o[r][2], __longlong_as_double(
+                                            (long long)(((uint64_t)(uint32_t)dest[r] << 32) |
+                                                        pid[r]))));
+        sts_row32(T.v, j, make_double2(o[r][3], o[r][4]), make_double2(o[r][5], m));
+        W.id[lane + 32 * r] = key[r];
+        leavers |= 1u << r;
+      }
     }
   }
   unsigned grp[R];
@@ -846,12 +859,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     for (int r = 0; r < R; ++r) {
       grp[r] = 0u;
       base[r] = 0u;
-      if (j0 + 32 * r < j1) {  // warp-uniform: every lane takes part in the ballot
-        if (decomposed(MODE))
-          send_foreign<MODE == kFused>(A, real[r] && !stay[r], dest[r], key[r], o[r], pid[r],
-                                       mm[r], acc[6]);
+      if (j0 + 32 * r < j1)  // warp-uniform: every lane takes part in the ballot
         claim_slot(A, stay[r], key[r], grp[r], base[r]);
-      }
     }
   }
   __syncwarp();
@@ -884,6 +893,30 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (stay[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
+  }
+  if (decomposed(MODE) && __any_sync(0xffffffffu, leavers != 0u)) {
+    // the pass's leavers, from their parked slots: one copy of the sending
+    // code, run only by passes that have any
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const bool go = (leavers >> r) & 1u;
+      double q[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, m = 0.0;
+      uint32_t id = 0u, k = 0u;
+      int to = 0;
+      if (go) {
+        double2 p01, p23, v01, v23;
+        lds_row32(T.p, j0 + lane + 32 * r, p01, p23);
+        lds_row32(T.v, j0 + lane + 32 * r, v01, v23);
+        const uint64_t bits = (uint64_t)__double_as_longlong(p23.y);
+        q[0] = p01.x; q[1] = p01.y; q[2] = p23.x; q[3] = v01.x; q[4] = v01.y; q[5] = v23.x;
+        m = v23.y;
+        id = (uint32_t)bits;
+        to = (int)(bits >> 32);
+        k = W.id[lane + 32 * r];
+      }
+      send_foreign<MODE == kFused>(A, go, to, k, q, id, m, acc[6]);
+    }
+    fence_proxy_async();  // the parked slots' generic writes precede the next TMA fill
   }
   if (DRIFT) {
     const int q = lane >> 2, comp = lane & 3;
