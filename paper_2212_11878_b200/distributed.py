@@ -499,9 +499,18 @@ class NcclRunner(_DomainRunner):
 def connect_fused(dom: "CudaDomain", exchange: DistExchange) -> bool:
     """Open every other rank's regions (CUDA IPC) for the fused migration.
     All ranks agree: if any rank fails, all fall back to the exchange."""
+    import torch
+
     err = None
+    # every peer's device must be reachable from this one (NVLink / P2P)
+    me = torch.cuda.current_device()
+    devices = exchange.gather_objects(me)
+    unreachable = [d for d in devices
+                   if d != me and not torch.cuda.can_device_access_peer(me, d)]
+    if unreachable:
+        err = f"device {me} cannot access peer device(s) {sorted(set(unreachable))}"
     try:
-        handles = dom.ctx.ipc_handles()
+        handles = dom.ctx.ipc_handles() if err is None else b""
     except Exception as e:  # noqa: BLE001 - reported, then the fallback
         err, handles = repr(e), b""
     allh = exchange.gather_objects(handles)
