@@ -299,7 +299,11 @@ __device__ __noinline__ double wrap_slow(double x, double box) { return wrap(x, 
 
 // particles.py:52-67 fast path (positions move less than a box per step)
 __device__ __forceinline__ double wrap_fast(double x, double box) {
-  if (x >= 0.0 && x < box) return x + 0.0;
+  // x in [+0, box): one unsigned compare of the bit patterns (box > 0, so
+  // -0.0, negatives and NaN all compare above); x is then its own remainder,
+  // already +0-signed (np.mod's copysign(0, box))
+  if ((unsigned long long)__double_as_longlong(x) < (unsigned long long)__double_as_longlong(box))
+    return x;
   if (x < 0.0 && x >= -box) {
     const double m = x + box;
     return (m == box) ? 0.0 : m;
