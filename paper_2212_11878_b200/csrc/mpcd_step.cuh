@@ -765,7 +765,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       double2 v01, v23;  // vx vy | vz m
       lds_row32(T.v, j0 + jl, v01, v23);
       const double m = UMASS ? A.m0 : v23.y;
-      sts_row32(W.val, row[r], make_double2(m * v01.x, m * v01.y), make_double2(m * v23.x, m));
+      if (UMASS && A.m0 == 1.0)  // unit masses: m v == v exactly, no multiplies
+        sts_row32(W.val, row[r], v01, make_double2(v23.x, 1.0));
+      else
+        sts_row32(W.val, row[r], make_double2(m * v01.x, m * v01.y), make_double2(m * v23.x, m));
     }
   }
   __syncwarp();
@@ -834,8 +837,11 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       else
         key[r] = BYID ? pid[r] : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
       const double m = mm[r];
-      sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]),
-                make_double2(m * w[2], m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2])));
+      const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
+      if (UMASS && A.m0 == 1.0)
+        sts_row32(W.val, row[r], make_double2(w[0], w[1]), make_double2(w[2], ke));
+      else
+        sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]), make_double2(m * w[2], m * ke));
       if (decomposed(MODE) && !stay[r]) {
         // a leaver: park its record in its own tile slot (dest in the pad
         // word) and its owner-local cell in W.id; flushed after the pass, so
