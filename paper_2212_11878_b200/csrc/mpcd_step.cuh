@@ -70,6 +70,9 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_PREFETCH_COUNTS
 #define MPCD_PREFETCH_COUNTS 0  // measured slower (7.55 vs 7.40 ms): off
 #endif
+#ifndef MPCD_BRANCHLESS4
+#define MPCD_BRANCHLESS4 1
+#endif
 #ifndef MPCD_CNT_EVICT_LAST
 #define MPCD_CNT_EVICT_LAST 1
 #endif
@@ -815,8 +818,15 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     key[r] = 0u;
     stay[r] = real[r];
     dest[r] = 0;
+#if MPCD_BRANCHLESS4
+    // padding lanes compute on a real slot of the pass (slot j0) and store
+    // nothing: no divergent region, so the rows' chains can interleave
+    {
+      const int j = real[r] ? j0 + lane + 32 * r : j0;
+#else
     if (real[r]) {
       const int j = j0 + lane + 32 * r;
+#endif
       double2 p01, p23, v01, v23;  // x y | z id, vx vy | vz m
       lds_row32(T.p, j, p01, p23);
       lds_row32(T.v, j, v01, v23);
@@ -833,16 +843,19 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       pid[r] = bits_id(p23.y);
       mm[r] = UMASS ? A.m0 : v23.y;
       if (decomposed(MODE))
-        stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]);
+        stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]) && real[r];
       else
         key[r] = BYID ? pid[r] : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
       const double m = mm[r];
       const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
-      if (UMASS && A.m0 == 1.0)
-        sts_row32(W.val, row[r], make_double2(w[0], w[1]), make_double2(w[2], ke));
-      else
-        sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]), make_double2(m * w[2], m * ke));
-      if (decomposed(MODE) && !stay[r]) {
+      if (real[r]) {
+        if (UMASS && A.m0 == 1.0)
+          sts_row32(W.val, row[r], make_double2(w[0], w[1]), make_double2(w[2], ke));
+        else
+          sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]),
+                    make_double2(m * w[2], m * ke));
+      }
+      if (decomposed(MODE) && real[r] && !stay[r]) {
         // a leaver: park its record in its own tile slot (dest in the pad
         // word) and its owner-local cell in W.id; flushed after the pass, so
         // the hot loop carries no copy of the sending code
