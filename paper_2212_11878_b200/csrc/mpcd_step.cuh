@@ -70,6 +70,9 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_PREFETCH_COUNTS
 #define MPCD_PREFETCH_COUNTS 0  // measured slower (7.55 vs 7.40 ms): off
 #endif
+#ifndef MPCD_EARLYCLAIM
+#define MPCD_EARLYCLAIM 1
+#endif
 #ifndef MPCD_BRANCHLESS4
 #define MPCD_BRANCHLESS4 1
 #endif
@@ -813,6 +816,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   bool stay[R];  // decomposed: the next cell is this domain's
   int dest[R];
   unsigned leavers = 0u;  // decomposed: bit r, row r's particle goes to another domain
+  unsigned grp[R];
+  uint32_t base[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     key[r] = 0u;
@@ -846,6 +851,13 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
         stay[r] = next_cell_multi<UNIT>(A, o[r][0], o[r][1], o[r][2], key[r], dest[r]) && real[r];
       else
         key[r] = BYID ? pid[r] : next_cell<UNIT>(A, o[r][0], o[r][1], o[r][2]);
+#if MPCD_EARLYCLAIM && MPCD_BRANCHLESS4
+      // claim as soon as the key is known: the atomic's round trip overlaps
+      // the staging below and the next row's whole chain
+      grp[r] = 0u;
+      base[r] = 0u;
+      if (!BYID && j0 + 32 * r < j1) claim_slot(A, stay[r], key[r], grp[r], base[r]);
+#endif
       const double m = mm[r];
       const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
       if (real[r]) {
@@ -869,15 +881,13 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       }
     }
   }
-  unsigned grp[R];
-  uint32_t base[R];
   if (BYID) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (real[r])
         store_rec(A.out, pid[r], o[r][0], o[r][1], o[r][2], pid[r], o[r][3], o[r][4], o[r][5],
                   mm[r]);
-  } else {
+  } else if (!(MPCD_EARLYCLAIM && MPCD_BRANCHLESS4)) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       grp[r] = 0u;
