@@ -64,9 +64,10 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
   else
     *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
-// Next-step counts stay in L2 (evict-last): their slot atomics are on the
-// critical path of every particle, and 40 % of them missed L2 with default
-// priority while the step streams its records through it.
+// Next-step counts carry an evict-last hint: their slot atomics are on the
+// critical path of every particle.  Measured 1 % faster than no hint,
+// although the atomics' L2 miss ratio (about 45 %, at every box size) is the
+// same either way (profiles/r01_k_step.md, v8).
 #ifndef MPCD_PREFETCH_COUNTS
 #define MPCD_PREFETCH_COUNTS 0  // measured slower (7.55 vs 7.40 ms): off
 #endif
@@ -527,9 +528,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ uint64_t policy_evict_first() {
+__device__ __forceinline__ uint64_t policy_evict_normal() {
   uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 // 1-D bulk copy global -> shared (TMA), completion counted on `bar`
@@ -990,7 +991,10 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   __syncthreads();
 
   if (warp == kNCW) {  // -------------------------------------- producer
-    const uint64_t pol = policy_evict_first();
+    // the records' TMA loads at evict-normal priority; measured slower:
+    // evict-first by 1.2 %, evict-last by 0.9 %, evict-first at fraction 0.5
+    // by 0.1 %; evict-unchanged is the same
+    const uint64_t pol = policy_evict_normal();
     int64_t tile = blockIdx.x;
     uint32_t cnt = tile_count(A, tile, ntiles);
     for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
