@@ -11,11 +11,12 @@ the reference's splitmix keyed RNG.  The particle state (17.4 GB with its
 double buffer) is far larger than L2, so no flush is needed between steps.
 
 `value` is timed with CUDA events around K back-to-back steps on the
-engine's stream (state resident in HBM).  `e2e` times the reference-facing
-pure function serial_collision_step through the C ABI (mpcd_step_host) on
-pinned HOST buffers: H2D of positions+velocities, binning, the step, D2H.
-`--impl reference` times the CPU oracle port (oracle/, the reference
-algorithm restated in C, all host threads) on a bounded sample.
+engine's stream (state resident in HBM).  `e2e` times the reference's public
+pure function serial_collision_step(p, params, k) chained on host rows: the
+rows go host -> device and back every step.  `--impl reference` times the
+reference algorithm on the host cores (the oracle, oracle/, its bit-exact C
+restatement, all host threads) on the same workload, and the reference
+package's own benchmark (baseline/_ref) on a 64^3 box beside it.
 """
 
 from __future__ import annotations
@@ -44,9 +45,10 @@ PPC = 10.0
 # cell read + zero its count and one atomic on the next count: 16 B) and the
 # compulsory floor B_min (read + write x, v once: 96 B).
 KERNELS = ("k_step", "k_step_dense", "k_diag")  # mpcd_read_profile slots 0..2
-# k_step, k_sort_dense, k_step_dense, k_diag_partial, k_diag_finalize
-# (+ k_place_xrecs, the absorb of received particles, in a decomposed box)
-LAUNCHES_PER_STEP = 5
+# k_step, k_dense_prep, k_ovf_bucket, k_step_dense, k_diag_partial,
+# k_diag_finalize (+ k_place_xrecs, the absorb of received particles, in a
+# decomposed box with the exchange migration)
+LAUNCHES_PER_STEP = 6
 BYTES_PER_N = {"k_step": 128, "k_step_dense": 0, "k_diag": 0}   # this design
 BYTES_PER_C = {"k_step": 16, "k_step_dense": 0, "k_diag": 0}
 SURVEY_B_ALG_N, SURVEY_B_ALG_C = 216, 28  # B_alg = 216 n + 28 C
@@ -183,11 +185,52 @@ def cpu_baseline(L, steps, seed):
                       f"{dt / steps:.3f} s/step"}
 
 
+def reference_package_cases(seed):
+    """The reference package's own benchmark (mpcdsim.bench.run_benchmark_case,
+    reference bench.py:77-122) on this host, when baseline/_ref holds its
+    offline install: the serial backend (1 core) and the process backend
+    (forked ranks, halo scheme) on a 64^3 box.  Secondary numbers beside the
+    oracle port; None when the package is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mpcdsim")):
+        return None
+    import math
+
+    sys.path.insert(0, ref)
+    try:
+        from mpcdsim import bench as rbench
+        from mpcdsim.params import SimParams as RParams
+    finally:
+        sys.path.remove(ref)
+    cpus = os.cpu_count() or 1
+    ranks = 1
+    while ranks * 2 <= min(cpus, 64):
+        ranks *= 2
+    out = {}
+    for name, backend, nranks in (("serial_64", "serial", 1), ("process_64", "process", ranks)):
+        params = RParams(edge_length=64, mean_density=PPC, dt=0.1, alpha=math.radians(130.0),
+                         seed=seed, n_steps=3, rank_dims=rbench.rank_dims_for(nranks))
+        t0 = time.perf_counter()
+        rec = rbench.run_benchmark_case(params, steps=2, warmup=1, backend=backend)
+        wall = time.perf_counter() - t0
+        out[name] = {"value": rec.particles * rec.steps / rec.seconds, "unit": UNIT,
+                     "cores": nranks, "backend": backend, "ranks": list(params.rank_dims),
+                     "seconds_per_step": rec.seconds / rec.steps, "wall_s": wall,
+                     "sample": "64^3 x 10 (2,621,440 particles), 1 warm-up + 2 timed steps"}
+    return out
+
+
 def run_reference(args):
+    """The reference's CPU implementation of the step on this host's cores
+    (the oracle: the reference algorithm restated in C, bit-exact with it,
+    all host threads) on the SAME workload as our arm -- args.L^3 cells x 10
+    -- with warm-up capped at 2 steps and the timed steps capped at ~240 s of
+    host work (the metric is a rate).  The reference package's own benchmark
+    runs beside it when installed (reference_package_cases)."""
     ws, rank, _ = dist_setup(args)
     if rank != 0:
         return
-    L = args.cpu_sample_L
+    L = args.L
     import numpy as np
 
     import oracle
@@ -196,30 +239,43 @@ def run_reference(args):
     pos, vel, mass = oracle.init_system(L, PPC, args.seed)
     n = pos.shape[0]
     cs, sn = float(np.cos(np.radians(130.0))), float(np.sin(np.radians(130.0)))
-    for k in range(args.warmup):
+    warm = min(args.warmup, 2)
+    t_warm = None
+    for k in range(warm):
+        t0 = time.perf_counter()
         r = oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, args.seed, k)
+        t_warm = time.perf_counter() - t0
         pos, vel = r.positions, r.velocities
+    timed = args.steps
+    if t_warm:
+        timed = max(1, min(args.steps, int(240.0 / t_warm)))
     t0 = time.perf_counter()
-    for k in range(args.warmup, args.warmup + args.steps):
+    for k in range(warm, warm + timed):
         r = oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, args.seed, k)
         pos, vel = r.positions, r.velocities
     dt = time.perf_counter() - t0
-    value = n * args.steps / dt
+    del pos, vel, r
+    value = n * timed / dt
+    sample = (f"{L}^3 cells x 10 ({n} particles) per step -- the benchmark workload itself -- "
+              f"{warm} warm-up + {timed} timed steps of the {args.steps} asked (capped at ~240 s "
+              f"of host work), {threads} OpenMP threads, oracle/mpcd_oracle.c (the reference "
+              "algorithm restated in C, bit-exact with the reference package)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / timed, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle init_system)",
-        "config": {"workload": f"{args.L}^3 cells x 10 particles/cell periodic SRD box, 130 deg, "
-                               f"dt 0.1, seed {args.seed} (timed on a {L}^3 sample)",
-                   "cells": L ** 3, "particles": n, "parallelism": "cpu"},
+        "config": {"workload": workload_text(args, 1, None),
+                   "cells_per_gpu": L ** 3, "particles_per_gpu": n, "parallelism": "cpu",
+                   "steps_timed": timed},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{L}^3 cells x 10 ({n} particles) per step, "
-                                   f"{threads} OpenMP threads; the reference package is pure "
-                                   "Python/numpy and is not installed on the GPU box, so its "
-                                   "bit-exact C restatement (oracle/) is timed"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["reference_package"] = reference_package_cases(args.seed)
+    except Exception as exc:  # noqa: BLE001 -- secondary numbers only
+        line["reference_package"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
 
 
@@ -384,6 +440,17 @@ def run_ours(args):
                       "collided": int(d.n), "migrated": int(d.migrated)},
     }
     line["clocks"] = clocks.summary()
+    if ws > 1:
+        # the migration over NVLink (fused) or NCCL (exchange): every particle
+        # that changes owner moves its two 32-byte records once
+        mig = [int(d.migrated)]
+        t = torch.tensor(mig, device="cuda", dtype=torch.int64)
+        torch.distributed.all_reduce(t)
+        line["migration"] = {"particles_per_step": int(t.item()),
+                             "bytes_per_step": 64 * int(t.item()),
+                             "bytes_per_gpu_per_step": 64 * int(d.migrated),
+                             "path": "NVLink peer stores inside k_step" if fused
+                             else "NCCL point-to-point"}
     if ws == 1 and not args.no_e2e:
         line["e2e"], line["e2e_stateful"] = e2e(args, params, ctx)
     elif ws > 1 and not args.no_e2e:
@@ -398,11 +465,13 @@ def run_ours(args):
 
 
 def workload_text(args, ws, params):
-    dims = "x".join(map(str, params.dims))
     if ws == 1:
+        L = args.L
+        dims = f"{L}x{L}x{L}"
         which = "BASELINE config 3" if args.L == 256 else "custom size"
         return (f"{dims} cells x 10 particles/cell periodic SRD box ({which}), 130 deg, dt 0.1, "
                 "splitmix keyed RNG")
+    dims = "x".join(map(str, params.dims))
     if args.config == 5:
         return (f"{dims} cells x 10 particles/cell (BASELINE config 5, strong scaling over "
                 f"{ws} GPUs), 130 deg, dt 0.1, splitmix keyed RNG")
@@ -439,48 +508,59 @@ def e2e_decomposed(args, params, dom, exch, fused):
 
 
 def e2e(args, params, ctx):
-    """Pure-function step through the C ABI on pinned host buffers, and the
-    stateful Simulation-style step with its per-step diagnostics read-back."""
+    """End to end through the public API, K steps each:
+
+    * ``e2e``: the reference's pure function ``serial_collision_step(p,
+      params, k)`` (engine.py:415-455) chained ``p = step(p)`` on host rows --
+      every step bins the caller's (n,3) rows from host memory over PCIe,
+      steps, and writes the new rows back to host memory (page-locked rows
+      from the API's own pool, read and written in place by the kernels);
+    * ``e2e_stateful``: ``Simulation.step()`` with the state resident in HBM
+      and the diagnostics read back every step.
+
+    The bench's own context is closed before the pure-function leg, which
+    builds its own (the API's cached context)."""
     import numpy as np
     import torch
 
+    from paper_2212_11878_b200 import ParticleSet, serial_collision_step
+
     n = params.n_particles
-    pos_t = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
-    vel_t = torch.empty((n, 3), dtype=torch.float64, pin_memory=True)
-    pos, vel = pos_t.numpy(), vel_t.numpy()
-    ids, p = ctx.download(id_order=True)
-    pos[:] = p.positions
-    vel[:] = p.velocities
-    del p, ids
-    step0 = 1000
-    ctx.step_host(pos, vel, None, step0, False)  # warm-up
-    torch.cuda.synchronize()
+    K = args.e2e_steps
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
-    K = args.e2e_steps
-    s.record()
-    for k in range(K):
-        ctx.step_host(pos, vel, None, step0 + 1 + k, False)
-    e.record()
-    torch.cuda.synchronize()
-    t = s.elapsed_time(e) * 1e-3
-    pure = {"value": n * K / t, "unit": UNIT, "h2d_bytes_per_step": 48 * n,
-            "d2h_bytes_per_step": 48 * n + 64,
-            "api": "mpcd_step_host == serial_collision_step(ParticleSet, params, step) on "
-                   "pinned host (n,3) float64 arrays"}
-    # stateful: Simulation.step() == mpcd_step + mpcd_read_diag (64 B D2H)
-    ctx.upload(pos, vel, None, None, step0 + K + 1)
+    # stateful: Simulation.step() == mpcd_step + mpcd_read_diag (diag + flags D2H)
+    first = int(ctx._lib.mpcd_current_step(ctx.handle))
     torch.cuda.synchronize()
     s.record()
     for k in range(args.steps):
-        ctx.step(step0 + K + 1 + k)
+        ctx.step(first + k)
         ctx.read_diag()
     e.record()
     torch.cuda.synchronize()
     t2 = s.elapsed_time(e) * 1e-3
     stateful = {"value": n * args.steps / t2, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 64, "api": "Simulation.step() (state resident, "
-                                                 "diagnostics read back every step)"}
+                "d2h_bytes_per_step": 72 + 64,
+                "api": "Simulation.step() (state resident, diagnostics read back every step)"}
+    ids, p = ctx.download(id_order=True)
+    del ids
+    ctx.close()
+    torch.cuda.empty_cache()
+    step0 = 1000
+    p, _, _ = serial_collision_step(p, params, step0)  # warm-up: context, pool, pageable input
+    torch.cuda.synchronize()
+    s.record()
+    for k in range(K):
+        p, _, _ = serial_collision_step(p, params, step0 + 1 + k)
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) * 1e-3
+    assert isinstance(p, ParticleSet) and p.n == n and np.isfinite(p.positions[-1]).all()
+    pure = {"value": n * K / t, "unit": UNIT, "h2d_bytes_per_step": 48 * n,
+            "d2h_bytes_per_step": 48 * n + 72 + 2 * 64,
+            "api": "serial_collision_step(ParticleSet, params, step) -- the reference's pure "
+                   "function -- chained p = step(p) on host (n,3) float64 rows (the API's pooled "
+                   "page-locked rows)", "steps": K}
     return pure, stateful
 
 

@@ -100,7 +100,9 @@ int mpcd_ctx_destroy(mpcd_ctx* ctx);
 
 /* Load n particles from HOST arrays in the reference layout: pos/vel (n,3)
  * float64 C-order, mass (n) float64 (ignored when uniform_mass), ids (n)
- * int64 (NULL = 0..n-1).  The state is then binned for step `step`. */
+ * int64 (NULL = 0..n-1).  The state is then binned for step `step`.  Ids
+ * must lie in [0, 2^32); a whole-box context requires a permutation of
+ * 0..n-1 (else MPCD_ERR_CONFIG). */
 int mpcd_upload(mpcd_ctx* ctx, const double* pos, const double* vel, const double* mass,
                 const int64_t* ids, int64_t n, int64_t step, void* stream);
 
@@ -113,6 +115,9 @@ int mpcd_download(mpcd_ctx* ctx, double* pos, double* vel, double* mass, int64_t
 int64_t mpcd_count(const mpcd_ctx* ctx);
 /* Record slots per cell region (fixed-capacity cell layout). */
 int64_t mpcd_cell_capacity(const mpcd_ctx* ctx);
+/* Cells per k_step tile (16, 8 or 4), chosen from capacity / cells so that
+ * tiles too full for shared-memory staging stay rare at any density. */
+int32_t mpcd_tile_cells(const mpcd_ctx* ctx);
 int64_t mpcd_current_step(const mpcd_ctx* ctx);
 
 /* One collision + streaming step with index `step` (the reference's
@@ -144,6 +149,22 @@ int mpcd_read_binning(mpcd_ctx* ctx, int64_t* cells, int64_t* bin_count, int64_t
  * NULL.  Uses ctx's device workspace (capacity >= n). */
 int mpcd_step_host(mpcd_ctx* ctx, double* pos, double* vel, const double* mass, int64_t n,
                    int64_t step, int32_t flags, double* drift, void* stream);
+
+/* Out-of-place form of mpcd_step_host: reads pos_in/vel_in, writes the
+ * stepped rows (input order) to pos_out/vel_out (which may alias the
+ * inputs).  Page-locked buffers (mpcd_host_alloc, cudaHostAlloc/Register)
+ * are read and written in place by the kernels over PCIe; pageable ones are
+ * staged through device memory. */
+int mpcd_step_rows(mpcd_ctx* ctx, const double* pos_in, const double* vel_in, const double* mass,
+                   int64_t n, int64_t step, int32_t flags, double* pos_out, double* vel_out,
+                   double* drift, void* stream);
+
+/* Page-locked, device-mapped host memory for the pure-function boundary's
+ * rows (the host shim pools these blocks), and whether a host pointer is
+ * page-locked (1) or pageable (0). */
+int mpcd_host_alloc(int64_t bytes, void** out);
+int mpcd_host_free(void* ptr);
+int mpcd_host_is_pinned(const void* ptr);
 
 /* Device init (particles.py:101-127 positions bit-exact; velocities are
  * Box-Muller with device log/cos, equal to numpy's only within ~1 ulp). */

@@ -47,6 +47,7 @@ from .engine import (
     POLICY_IMMEDIATE,
     POLICY_LAZY,
     ConservationReport,
+    DecompositionAliasWarning,
     EquivalenceReport,
     Simulation,
     conservation_report,

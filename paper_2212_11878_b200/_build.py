@@ -22,7 +22,6 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
-    "-shared",
 ]
 
 
@@ -47,19 +46,47 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines=None, out: str | None = None) -> str:
-    """Compile libmpcd.so (or a tuning variant with -D`defines` into `out`)."""
+    """Compile libmpcd.so (or a tuning variant with -D`defines` into `out`).
+
+    Each translation unit (the engine, the scan, the stage kernels and the
+    four step-mode variant units) compiles in its own nvcc process, in
+    parallel; the objects are then linked into the shared library."""
+    import concurrent.futures as cf
+    import tempfile
+
     target = out or LIB
     if not force and out is None and not needs_build():
         return LIB
     flags = [f"-D{d}" for d in (defines or [])]
-    cmd = [nvcc(), *NVCC_FLAGS, *flags, "-I", INCLUDE, "-I", CSRC, "-o", target + ".tmp", *sources()]
-    env = dict(os.environ)
+    base = [nvcc()]
     # the distro g++ is the host compiler nvcc 12.9 supports here
     if os.path.exists("/usr/bin/g++"):
-        cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True, env=env)
+        base += ["-ccbin", "/usr/bin/g++"]
+    with tempfile.TemporaryDirectory(prefix="mpcd_build_") as tmp:
+        jobs = []
+        for src in sources():
+            obj = os.path.join(tmp, os.path.basename(src)[:-3] + ".o")
+            jobs.append((obj, [*base, *NVCC_FLAGS, *flags, "-I", INCLUDE, "-I", CSRC,
+                               "-c", "-o", obj, src]))
+        if verbose:
+            for _, cmd in jobs:
+                print(" ".join(cmd))
+
+        def run(cmd):
+            return subprocess.run(cmd, capture_output=True, text=True)
+
+        with cf.ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            results = list(ex.map(run, [cmd for _, cmd in jobs]))
+        for (_, cmd), r in zip(jobs, results):
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{r.stdout}{r.stderr}")
+            if verbose and (r.stdout or r.stderr):
+                print(r.stdout + r.stderr)
+        link = [*base, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                "-o", target + ".tmp", *[obj for obj, _ in jobs]]
+        if verbose:
+            print(" ".join(link))
+        subprocess.run(link, check=True)
     os.replace(target + ".tmp", target)
     return target
 

@@ -83,6 +83,7 @@ SIGNATURES = {
     "mpcd_download": (C.c_int, [_vp, _d, _d, _d, _i64, C.c_int32, _vp]),
     "mpcd_count": (C.c_int64, [_vp]),
     "mpcd_cell_capacity": (C.c_int64, [_vp]),
+    "mpcd_tile_cells": (C.c_int32, [_vp]),
     "mpcd_current_step": (C.c_int64, [_vp]),
     "mpcd_step": (C.c_int, [_vp, C.c_int64, C.c_int32, _vp]),
     "mpcd_run": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int32, _vp]),
@@ -90,6 +91,11 @@ SIGNATURES = {
     "mpcd_read_com": (C.c_int, [_vp, _i64, _d, _i64, _vp]),
     "mpcd_read_binning": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _vp]),
     "mpcd_step_host": (C.c_int, [_vp, _d, _d, _d, C.c_int64, C.c_int64, C.c_int32, _d, _vp]),
+    "mpcd_step_rows": (C.c_int, [_vp, _d, _d, _d, C.c_int64, C.c_int64, C.c_int32, _d, _d, _d,
+                                 _vp]),
+    "mpcd_host_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    "mpcd_host_free": (C.c_int, [_vp]),
+    "mpcd_host_is_pinned": (C.c_int, [_vp]),
     "mpcd_init_device": (C.c_int, [_vp, C.c_int64, C.c_double, C.c_int64, _vp]),
     "mpcd_ctx_set_domain": (C.c_int, [_vp, C.POINTER(MpcdDomain)]),
     "mpcd_exchange_buffers": (C.c_int, [_vp, C.POINTER(MpcdExchange)]),

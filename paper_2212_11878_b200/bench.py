@@ -1,33 +1,34 @@
-"""Scaling benchmark over a (size, ranks) matrix, in the reference's CSV
-format (mpcdsim/bench.py:1-243).
+"""The reference's scaling-benchmark report on the
+GPU backends.
 
-Same names, arguments, columns and error behaviour as the reference.
-`backend` selects this package's backends:
+Drop-in surface of ``mpcdsim.bench`` (reference bench.py:1-243): the names
+``BenchRecord``, ``CSV_COLUMNS``, ``rank_dims_for``, ``run_benchmark_case``,
+``run_benchmark_matrix``, ``emit_report`` and ``read_report``, with the same
+arguments, the same CSV file (header + one row per case, floats written with
+``repr`` so they read back exactly) and the same ``<path>.summary.txt`` lines.
 
-- one rank: ``"cuda"``;
-- several: ``"sequential"`` (every domain on this GPU), or ``"nccl"`` under
-  torchrun.
+What differs is what is timed and counted:
 
-The reference counts its in-process Transport's messages. Here the traffic
-columns count what actually moves between domains each step:
-
-- `bytes_per_step` is the migrated particles times the 64-byte record;
-- `msgs_per_step` is the number of domains that sent particles. With the
-  fused migration each such domain writes straight into its neighbours'
-  cells.
-
-There are no moment messages: a cell is never split between domains
-(DESIGN.md section 6).
+* a case runs on ``"cuda"`` (one domain) or, for several ranks, on
+  ``"sequential"`` (every domain on this GPU) or ``"nccl"`` (torchrun);
+  each measured step is bracketed by CUDA events on the engine's stream;
+* the traffic columns count the particle migration, the only inter-domain
+  traffic of the cell-ownership decomposition:
+  ``bytes_per_step`` = migrated particles x the 64-byte record, and
+  ``msgs_per_step`` = domains that sent particles.  No cell is ever split,
+  so there are no moment messages.
 """
 
 from __future__ import annotations
 
 import csv
-import time
-from dataclasses import dataclass, fields
+import heapq
+import itertools
+from dataclasses import astuple, dataclass, fields
 
 import numpy as np
 
+from . import _dev
 from .engine import BACKEND_CUDA, BACKEND_SEQUENTIAL, Simulation
 from .errors import ConfigError, MpcdError
 from .params import SCHEME_HALO, SimParams
@@ -35,7 +36,7 @@ from .params import SCHEME_HALO, SimParams
 DEFAULT_SIZES = (16, 32, 64)
 DEFAULT_RANK_COUNTS = (1, 2, 4, 8)
 DEFAULT_WARMUP = 5
-RECORD_BYTES = 64
+RECORD_BYTES = 64  # one migrated particle: two 32-byte records
 
 CSV_COLUMNS = ("L", "ranks", "scheme", "steps", "seconds", "particles", "bytes_per_step",
                "msgs_per_step", "max_drift", "error")
@@ -43,6 +44,8 @@ CSV_COLUMNS = ("L", "ranks", "scheme", "steps", "seconds", "particles", "bytes_p
 
 @dataclass
 class BenchRecord:
+    """One (size, scheme, ranks) case; ``error`` is empty unless it failed."""
+
     L: int
     ranks: int
     scheme: str
@@ -54,57 +57,91 @@ class BenchRecord:
     max_drift: float
     error: str = ""
 
+    @classmethod
+    def failed(cls, L: int, ranks: int, scheme: str, steps: int, exc: BaseException):
+        return cls(L, ranks, scheme, steps, 0.0, 0, 0.0, 0.0, 0.0,
+                   f"{type(exc).__name__}: {exc}")
+
+
+# ------------------------------------------------------------- ranks ---
+def _prime_factors(n: int):
+    p = 2
+    while p * p <= n:
+        while n % p == 0:
+            yield p
+            n //= p
+        p += 1 if p == 2 else 2
+    if n > 1:
+        yield n
+
 
 def rank_dims_for(n_ranks: int) -> tuple:
-    """Near-cubic 3-d factorisation of a rank count (bench.py:53-74): prime
-    factors, largest first, each to the currently smallest dimension."""
+    """Near-cubic (x, y, z) rank grid for ``n_ranks`` (descending).
+
+    The reference's rule (bench.py:53-74): hand the prime factors out,
+    largest first, each to the axis that is currently smallest (the first
+    such axis on ties).  A heap of (extent, axis) does the bookkeeping.
+    """
     if n_ranks < 1:
         raise ConfigError("rank count must be positive")
-    factors = []
-    n, d = n_ranks, 2
-    while d * d <= n:
-        while n % d == 0:
-            factors.append(d)
-            n //= d
-        d += 1
-    if n > 1:
-        factors.append(n)
-    dims = [1, 1, 1]
-    for f in sorted(factors, reverse=True):
-        dims[int(np.argmin(dims))] *= f
-    dims.sort(reverse=True)
-    return (dims[0], dims[1], dims[2])
+    heap = [(1, axis) for axis in range(3)]
+    for f in sorted(_prime_factors(n_ranks), reverse=True):
+        extent, axis = heapq.heappop(heap)
+        heapq.heappush(heap, (extent * f, axis))
+    return tuple(sorted((extent for extent, _ in heap), reverse=True))
+
+
+# ------------------------------------------------------------ timing ---
+class _StepClock:
+    """CUDA events around each measured step on the engine's stream."""
+
+    def __init__(self):
+        torch = _dev.torch()
+        self._torch = torch
+        self._pairs = []
+
+    def time(self, fn):
+        torch = self._torch
+        stream = torch.cuda.current_stream()
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        out = fn()
+        stop.record(stream)
+        self._pairs.append((start, stop))
+        return out
+
+    def seconds(self) -> float:
+        self._torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in self._pairs) / 1e3
 
 
 def run_benchmark_case(params: SimParams, *, steps: int, warmup: int = DEFAULT_WARMUP,
                        backend: str = BACKEND_SEQUENTIAL) -> BenchRecord:
-    """Time `steps` steps after `warmup` unmeasured ones (bench.py:77-122)."""
+    """Warm up, then time ``steps`` steps of one configuration
+    (reference bench.py:77-122).  ``max_drift`` is the largest deviation of
+    the total momentum from its post-warm-up value over the measured steps."""
     if steps < 1:
         raise ConfigError("bench needs at least one measured step")
-    if params.n_ranks == 1:
-        backend = BACKEND_CUDA
-    sim = Simulation(params, backend=backend)
-    try:
-        sim.run(warmup)
-        p_ref = sim.conservation_report().total_momentum
-        max_drift = 0.0
-        seconds = 0.0
-        moved = 0
-        senders = 0
+    chosen = BACKEND_CUDA if params.n_ranks == 1 else backend
+    with Simulation(params, backend=chosen) as sim:
+        for _ in range(warmup):
+            sim.step()
+        momentum0 = np.asarray(sim.conservation_report().total_momentum, dtype=np.float64)
+        clock = _StepClock()
+        migrated = senders = 0
+        drift = 0.0
         for _ in range(steps):
-            t0 = time.perf_counter()
-            diag = sim.step()  # synchronises: the diagnostics are read back
-            seconds += time.perf_counter() - t0
-            moved += int(diag.get("crossings", 0))
+            diag = clock.time(sim.step)
+            migrated += int(diag.get("crossings", 0))
             senders += int(diag.get("sending_domains", 0))
-            mom = sim.conservation_report().total_momentum
-            max_drift = max(max_drift, float(np.max(np.abs(mom - p_ref))))
+            now = np.asarray(sim.conservation_report().total_momentum, dtype=np.float64)
+            drift = max(drift, float(np.abs(now - momentum0).max()))
         return BenchRecord(L=params.edge_length, ranks=params.n_ranks, scheme=params.scheme,
-                           steps=steps, seconds=seconds, particles=params.n_particles,
-                           bytes_per_step=moved * RECORD_BYTES / steps,
-                           msgs_per_step=senders / steps, max_drift=max_drift)
-    finally:
-        sim.close()
+                           steps=steps, seconds=clock.seconds(),
+                           particles=params.n_particles,
+                           bytes_per_step=RECORD_BYTES * migrated / steps,
+                           msgs_per_step=senders / steps, max_drift=drift)
 
 
 def run_benchmark_matrix(sizes=DEFAULT_SIZES, rank_counts=DEFAULT_RANK_COUNTS,
@@ -113,77 +150,76 @@ def run_benchmark_matrix(sizes=DEFAULT_SIZES, rank_counts=DEFAULT_RANK_COUNTS,
                          cell_size: float = 1.0, dt: float = 0.1, alpha_degrees: float = 130.0,
                          halo_width: int = 1, seed: int = 0, backend: str = BACKEND_SEQUENTIAL,
                          progress=None) -> list:
-    """Every (size, scheme, ranks) case; a failing case becomes an error row
-    and the matrix goes on (bench.py:125-182)."""
-    records = []
-    for L in sizes:
-        for scheme in schemes:
-            for ranks in rank_counts:
-                if progress is not None:
-                    progress(L, scheme, ranks)
-                try:
-                    params = SimParams(edge_length=L, cell_size=cell_size, mean_density=density,
-                                       dt=dt, alpha=np.radians(alpha_degrees),
-                                       halo_width=halo_width, seed=seed, n_steps=steps,
-                                       scheme=scheme, rank_dims=rank_dims_for(ranks))
-                    records.append(run_benchmark_case(params, steps=steps, warmup=warmup,
-                                                      backend=backend))
-                except Exception as exc:  # keep the matrix going
-                    records.append(BenchRecord(L=L, ranks=ranks, scheme=scheme, steps=steps,
-                                               seconds=0.0, particles=0, bytes_per_step=0.0,
-                                               msgs_per_step=0.0, max_drift=0.0,
-                                               error=f"{type(exc).__name__}: {exc}"))
-    return records
+    """Every (size, scheme, ranks) case in that nesting order; a case that
+    raises becomes an error record and the matrix carries on
+    (reference bench.py:125-182)."""
+    out = []
+    for L, scheme, ranks in itertools.product(sizes, schemes, rank_counts):
+        if progress is not None:
+            progress(L, scheme, ranks)
+        try:
+            params = SimParams(edge_length=L, cell_size=cell_size, mean_density=density, dt=dt,
+                               alpha=float(np.radians(alpha_degrees)), halo_width=halo_width,
+                               seed=seed, n_steps=steps, scheme=scheme,
+                               rank_dims=rank_dims_for(ranks))
+            out.append(run_benchmark_case(params, steps=steps, warmup=warmup, backend=backend))
+        except Exception as exc:  # noqa: BLE001 -- recorded, not raised
+            out.append(BenchRecord.failed(L, ranks, scheme, steps, exc))
+    return out
 
 
-def _cell_text(value) -> str:
+# ------------------------------------------------------------ report ---
+_COLUMN_TYPES = {f.name: f.type for f in fields(BenchRecord)}
+_PARSERS = {"int": int, "float": float, "str": str, int: int, float: float, str: str}
+
+
+def _encode(value) -> str:
+    # repr for floats: the CSV must read back bit for bit
     return repr(value) if isinstance(value, float) else str(value)
 
 
+def _summary_lines(records):
+    serial = {(r.L, r.scheme): r.seconds for r in records
+              if r.ranks == 1 and not r.error and r.seconds > 0}
+    for r in records:
+        head = f"L={r.L} scheme={r.scheme} ranks={r.ranks}"
+        if r.error:
+            yield f"{head} FAILED: {r.error}"
+            continue
+        text = (f"{head} seconds={r.seconds:.3f} bytes/step={r.bytes_per_step:.0f} "
+                f"msgs/step={r.msgs_per_step:.1f}")
+        one = serial.get((r.L, r.scheme))
+        if one is not None and r.seconds > 0:
+            text += f" speedup={one / r.seconds:.2f}"
+        yield text
+
+
 def emit_report(records: list, path: str) -> None:
-    """The CSV plus a human-readable speedup summary (bench.py:191-222)."""
+    """``path``: the CSV; ``path + ".summary.txt"``: one line per case with
+    the speed-up over the same size's one-rank case (bench.py:191-222)."""
     if not records:
         raise MpcdError("benchmark produced no records")
+    order = [CSV_COLUMNS.index(f.name) for f in fields(BenchRecord)]
     with open(path, "w", newline="") as fh:
-        writer = csv.writer(fh)
-        writer.writerow(CSV_COLUMNS)
+        out = csv.writer(fh)
+        out.writerow(CSV_COLUMNS)
         for rec in records:
-            writer.writerow([_cell_text(getattr(rec, name)) for name in CSV_COLUMNS])
+            cells = [""] * len(CSV_COLUMNS)
+            for pos, value in zip(order, astuple(rec)):
+                cells[pos] = _encode(value)
+            out.writerow(cells)
     with open(path + ".summary.txt", "w") as fh:
-        base = {}
-        for rec in records:
-            if rec.ranks == 1 and not rec.error and rec.seconds > 0:
-                base[(rec.L, rec.scheme)] = rec.seconds
-        for rec in records:
-            if rec.error:
-                fh.write(f"L={rec.L} scheme={rec.scheme} ranks={rec.ranks} FAILED: {rec.error}\n")
-                continue
-            line = (f"L={rec.L} scheme={rec.scheme} ranks={rec.ranks} seconds={rec.seconds:.3f}"
-                    f" bytes/step={rec.bytes_per_step:.0f} msgs/step={rec.msgs_per_step:.1f}")
-            ref = base.get((rec.L, rec.scheme))
-            if ref is not None and rec.seconds > 0:
-                line += f" speedup={ref / rec.seconds:.2f}"
-            fh.write(line + "\n")
+        fh.writelines(line + "\n" for line in _summary_lines(records))
 
 
 def read_report(path: str) -> list:
-    """Records back from a CSV written by emit_report, floats exact (repr)
-    (bench.py:225-243)."""
-    types = {f.name: f.type for f in fields(BenchRecord)}
-    out = []
+    """The records of a CSV written by ``emit_report`` (bench.py:225-243);
+    any other header is an MpcdError."""
     with open(path, newline="") as fh:
-        reader = csv.DictReader(fh)
-        if tuple(reader.fieldnames or ()) != CSV_COLUMNS:
+        rows = csv.reader(fh)
+        header = tuple(next(rows, ()))
+        if header != CSV_COLUMNS:
             raise MpcdError(f"unexpected benchmark columns in {path}")
-        for row in reader:
-            kw = {}
-            for name in CSV_COLUMNS:
-                typ, raw = types[name], row[name]
-                if typ in (int, "int"):
-                    kw[name] = int(raw)
-                elif typ in (float, "float"):
-                    kw[name] = float(raw)
-                else:
-                    kw[name] = raw
-            out.append(BenchRecord(**kw))
-    return out
+        parse = [_PARSERS[_COLUMN_TYPES[name]] for name in header]
+        return [BenchRecord(**{name: conv(cell) for name, conv, cell in zip(header, parse, row)})
+                for row in rows]

@@ -32,6 +32,7 @@
 
 #include "mpcd_internal.h"
 #include "mpcd_step.cuh"
+#include "mpcd_launch.cuh"
 
 namespace mpcd {
 
@@ -350,6 +351,9 @@ struct mpcd_ctx {
   mpcd_config cfg;
   int64_t C = 0, ntiles = 0, n = 0;
   uint32_t cap = 0, ovf_cap = 0, scratch_cap = 0;
+  int tc = kTC;            // cells per tile of k_step (chosen from the density)
+  uint32_t np_smem = 0;    // dense-tile particles staged in shared memory
+  bool poisoned = false;   // particles were lost (capacity): steps refuse
   int dev = 0;
   void* slab[2] = {nullptr, nullptr};
   Recs reg[2];
@@ -357,8 +361,13 @@ struct mpcd_ctx {
   void* ovf_slab[2] = {nullptr, nullptr};
   Recs ovf[2];
   uint32_t* ovf_cell[2] = {nullptr, nullptr};
-  uint32_t* small = nullptr;  // [0..3] flags, [4,5] ovf_n, [6] scratch_n
+  // [0..3] flags, [4,5] ovf_n, [6] scratch_n, [7] placed, [8] overflow
+  // bucket allocator, [9] dense staging exhausted
+  uint32_t* small = nullptr;
   uint32_t* dense = nullptr;
+  uint32_t* dense_bits = nullptr;
+  uint32_t* cell_aux = nullptr;
+  uint32_t* ovf_sorted = nullptr;
   uint32_t* scratch_id = nullptr;
   uint32_t* scratch_src = nullptr;
   double* scratch_val = nullptr;
@@ -399,6 +408,10 @@ uint32_t* flags_of(mpcd_ctx* c) { return c->small; }
 uint32_t* ovf_n_of(mpcd_ctx* c, int b) { return c->small + 4 + b; }
 uint32_t* scratch_n_of(mpcd_ctx* c) { return c->small + 6; }
 uint32_t* placed_of(mpcd_ctx* c) { return c->small + 7; }
+constexpr int kSmallWords = 16;
+
+// partials rows: k_step's CTAs first, then one row per tile of k_step_dense
+constexpr int64_t kMainRows = 4096;
 
 struct DeviceGuard {
   int prev = -1;
@@ -416,6 +429,23 @@ Recs carve(void* slab, uint64_t rows) {
   r.p = static_cast<PRec*>(slab);
   r.v = reinterpret_cast<VRec*>(static_cast<char*>(slab) + sizeof(PRec) * rows);
   return r;
+}
+
+// Cells per k_step tile: the largest multiple of kNCW (one consumer-warp
+// share each) up to kTC whose padded tile (cells padded to 4 slots, ~1.5 per
+// cell) stays within the kMaxPT staging slots with 2.5 standard deviations
+// to spare -- so that dense tiles stay rare (measured: a few per mille of
+// the tiles cost far less than the lane utilisation a smaller tile loses).
+// 16 cells at 10 particles per cell; 8 from ~17; 4 from ~27.
+// MPCD_TILE_CELLS overrides it (tuning and tests).
+int tile_cells(double density) {
+  if (const char* e = getenv("MPCD_TILE_CELLS")) {
+    const int v = atoi(e);
+    if (v >= kNCW && v <= kTC && v % kNCW == 0) return v;
+  }
+  for (int tc = kTC; tc > kNCW; tc -= kNCW)
+    if (tc * (density + 1.5) + 2.5 * sqrt(tc * density) <= (double)kMaxPT) return tc;
+  return kNCW;
 }
 
 // Poisson-tail default: the smallest multiple of 8 with an expected number of
@@ -474,6 +504,37 @@ T* mapped(T* p) {
   if (a.type == cudaMemoryTypeHost && a.devicePointer) return static_cast<T*>(a.devicePointer);
   if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return p;
   return nullptr;
+}
+
+// Particle ids are stored as u32; a whole-box context also writes row `id`
+// of an n-row array when it downloads in id order, so its ids must be a
+// permutation of 0..n-1 (a decomposed domain holds a subset of the global
+// ids and sorts them on the host instead).
+int validate_ids(const int64_t* ids, int64_t n, bool permutation) {
+  std::vector<int64_t> copy;
+  const int64_t* h = ids;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ids) != cudaSuccess) {
+    cudaGetLastError();
+  } else if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    copy.resize(n);
+    MPCD_CUDA(cudaMemcpy(copy.data(), ids, sizeof(int64_t) * n, cudaMemcpyDefault));
+    h = copy.data();
+  }
+  std::vector<uint8_t> seen(permutation ? n : 0, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t id = h[i];
+    if (id < 0 || id >= (1LL << 32))
+      return fail(MPCD_ERR_CONFIG, "particle id %lld (row %lld) outside [0, 2^32)", (long long)id,
+                  (long long)i);
+    if (permutation) {
+      if (id >= n || seen[id])
+        return fail(MPCD_ERR_CONFIG, "ids of a whole-box context must be a permutation of "
+                    "0..n-1 (row %lld has id %lld)", (long long)i, (long long)id);
+      seen[id] = 1;
+    }
+  }
+  return MPCD_OK;
 }
 
 // Refresh c->n after fused steps (peers added and removed particles).
@@ -560,17 +621,24 @@ int ensure_binned(mpcd_ctx* c, int64_t step, cudaStream_t st) {
 }
 
 int check_flags(mpcd_ctx* c, cudaStream_t st) {
-  uint32_t fl[4];
+  uint32_t fl[kSmallWords];
   MPCD_CUDA(cudaMemcpyAsync(fl, flags_of(c), sizeof(fl), cudaMemcpyDeviceToHost, st));
   MPCD_CUDA(cudaStreamSynchronize(st));
-  if (fl[1] || fl[2] || fl[3]) {
+  if (fl[1] || fl[2] || fl[3] || fl[9]) {
     cudaMemsetAsync(flags_of(c) + 1, 0, 3 * sizeof(uint32_t), st);
+    cudaMemsetAsync(flags_of(c) + 9, 0, sizeof(uint32_t), st);
     if (fl[1]) return fail(MPCD_ERR_RNG, "axis rejection sampling failed to terminate");
     if (fl[3])
       return fail(MPCD_ERR_TOPOLOGY, "a particle given to domain %d lies outside its cells",
                   (int)c->dom.rank);
+    c->poisoned = true;  // particles were dropped: the state is no longer the system
+    if (fl[9])
+      return fail(MPCD_ERR_CAPACITY, "a cluster of full tiles exceeds the dense-tile staging "
+                                     "capacity (%u particles); particles were lost",
+                  c->scratch_cap);
     return fail(MPCD_ERR_CAPACITY, "overflow list full: more particles in full cells than the "
-                                   "context's overflow capacity %u", c->ovf_cap);
+                                   "context's overflow capacity %u; particles were lost",
+                c->ovf_cap);
   }
   return MPCD_OK;
 }
@@ -596,10 +664,17 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.drift_bits = c->drift_bits;
   A.flags = flags_of(c);
   A.dense = c->dense;
+  A.dense_bits = c->dense_bits;
+  A.cell_aux = c->cell_aux;
+  A.ovf_sorted = c->ovf_sorted;
   A.scratch_n = scratch_n_of(c);
   A.scratch_id = c->scratch_id;
   A.scratch_val = c->scratch_val;
   A.scratch_src = c->scratch_src;
+  A.scratch_cap = c->scratch_cap;
+  A.np_smem = c->np_smem;
+  A.tc = c->tc;
+  A.cw = c->tc / kNCW;
   A.L0 = (int)g.dims[0]; A.L1 = (int)g.dims[1]; A.L2 = (int)g.dims[2];
   A.C = c->C;
   A.a = g.cell_size;
@@ -617,7 +692,7 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.prng = g.prng;
   A.axis_prefix = key_prefix(g.seed, (uint64_t)step, kAxis);
   A.m0 = g.mass_value;
-  A.part_base = 0;
+  A.dense_row0 = kMainRows;
   (void)by_id;
   A.peers = c->p2p ? c->d_peers : nullptr;
   A.out_set = b ^ 1;
@@ -643,76 +718,21 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   return A;
 }
 
-// Resident CTAs per device for a persistent kernel, cached per (kernel, device).
-int64_t resident_ctas(const void* kernel, int block, size_t smem) {
-  static std::map<std::pair<const void*, int>, int64_t> cache;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  auto key = std::make_pair(kernel, dev);
-  auto it = cache.find(key);
-  if (it == cache.end()) {
-    int sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
-    it = cache.emplace(key, (int64_t)std::max(per_sm, 1) * sms).first;
-  }
-  return it->second;
-}
-
-constexpr int64_t kDenseGrid = 592;
-
-// which == 0: the persistent tile kernel (returns its grid); which == 1: the
-// dense-tile kernel after sorting its tile list.
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
-int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_t st) {
-  if (which == 0) {
-    auto kern = k_step<UNIT, UMASS, DRIFT, COM, MODE>;
-    const size_t smem = sizeof(StepSmem<DRIFT>);
-    const int64_t grid =
-        std::max<int64_t>(1, std::min<int64_t>(ntiles, resident_ctas((const void*)kern, kNTW, smem)));
-    kern<<<(unsigned)grid, kNTW, smem, st>>>(A, ntiles);
-    return grid;
-  }
-  k_sort_dense<<<1, 1, 0, st>>>(A.dense, A.flags);
-  k_step_dense<UNIT, UMASS, DRIFT, COM, MODE><<<(unsigned)kDenseGrid, kNT, 0, st>>>(A);
-  return kDenseGrid;
-}
-
-// 64 compile-time variants, chosen at run time
-struct Variant {
-  bool unit, umass, drift, com;
-  int mode;
-};
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM>
-int64_t launch_mode(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.mode == kById) return launch_variant<UNIT, UMASS, DRIFT, COM, kById>(A, nt, which, st);
-  if (v.mode == kMulti) return launch_variant<UNIT, UMASS, DRIFT, COM, kMulti>(A, nt, which, st);
-  if (v.mode == kFused) return launch_variant<UNIT, UMASS, DRIFT, COM, kFused>(A, nt, which, st);
-  return launch_variant<UNIT, UMASS, DRIFT, COM, kBinned>(A, nt, which, st);
-}
-template <bool UNIT, bool UMASS, bool DRIFT>
-int64_t launch_com(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.com) return launch_mode<UNIT, UMASS, DRIFT, true>(A, nt, v, which, st);
-  return launch_mode<UNIT, UMASS, DRIFT, false>(A, nt, v, which, st);
-}
-template <bool UNIT, bool UMASS>
-int64_t launch_drift(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.drift) return launch_com<UNIT, UMASS, true>(A, nt, v, which, st);
-  return launch_com<UNIT, UMASS, false>(A, nt, v, which, st);
-}
+// The k_step / k_step_dense variants are compiled in four translation units,
+// one per step mode (mpcd_step_<mode>.cu, built in parallel).
 int64_t launch_step_kernel(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
-  if (v.unit) {
-    if (v.umass) return launch_drift<true, true>(A, nt, v, which, st);
-    return launch_drift<true, false>(A, nt, v, which, st);
+  switch (v.mode) {
+    case kById: return launch_mode_byid(A, nt, v, which, st);
+    case kMulti: return launch_mode_multi(A, nt, v, which, st);
+    case kFused: return launch_mode_fused(A, nt, v, which, st);
+    default: return launch_mode_binned(A, nt, v, which, st);
   }
-  if (v.umass) return launch_drift<false, true>(A, nt, v, which, st);
-  return launch_drift<false, false>(A, nt, v, which, st);
 }
 
 int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t st) {
+  if (c->poisoned)
+    return fail(MPCD_ERR_CAPACITY, "the context lost particles in an earlier step (capacity "
+                "exceeded); upload or initialise the state again");
   if (c->multi && !(c->binned && c->cur_step == step))
     return fail(MPCD_ERR_CONFIG, "a decomposed domain steps consecutively: it holds the "
                 "particles of step %lld's cells, not of step %lld's",
@@ -735,12 +755,18 @@ int launch_step(mpcd_ctx* c, int64_t step, int flags, bool by_id, cudaStream_t s
                   by_id ? kById : (c->multi ? (c->p2p ? kFused : kMulti) : kBinned)};
   const int64_t grid = launch_step_kernel(A, c->ntiles, v, 0, st);
   MPCD_LAUNCH_CHECK();
+  if (grid > kMainRows) return fail(MPCD_ERR_CUDA, "step grid %lld exceeds its partials rows",
+                                    (long long)grid);
   if (ev) MPCD_CUDA(cudaEventRecord(ev[1], st));
-  A.part_base = grid;  // the dense CTAs' partial rows follow the tile kernel's
-  const int64_t nparts = grid + launch_step_kernel(A, c->ntiles, v, 1, st);
+  // the dense-tile path: overflow buckets, then the dense-tile kernel (each
+  // exits at once when k_step queued no tile)
+  k_dense_prep<<<grid_for(c->ntiles, 256, kDenseGrid), 256, 0, st>>>(A);
+  k_ovf_bucket<<<(unsigned)kDenseGrid, 256, 0, st>>>(A);
+  launch_step_kernel(A, c->ntiles, v, 1, st);
   MPCD_LAUNCH_CHECK();
   if (ev) MPCD_CUDA(cudaEventRecord(ev[2], st));
-  k_diag_partial<<<kDiagBlocks, 256, 0, st>>>(c->partials, nparts, c->level1);
+  k_diag_partial<<<kDiagBlocks, 256, 0, st>>>(c->partials, grid, kMainRows, c->ntiles,
+                                              c->dense_bits, flags_of(c), c->level1);
   MPCD_LAUNCH_CHECK();
   k_diag_finalize<<<1, 32, 0, st>>>(c->level1, kDiagBlocks, c->drift_bits, c->diag, step,
                                     flags_of(c), ovf_n_of(c, c->cur), scratch_n_of(c));
@@ -876,14 +902,38 @@ int mpcd_ctx_create(const mpcd_config* cfg, mpcd_ctx** out) {
   c->cfg = *cfg;
   c->dev = cfg->device;
   c->C = C;
-  c->ntiles = (C + kTC - 1) / kTC;
   const int64_t cap_n = std::max<int64_t>(cfg->capacity, 1);
+  const double density = (double)cap_n / (double)C;
+  c->tc = tile_cells(density);
+  c->ntiles = (C + c->tc - 1) / c->tc;
+  // dense tiles of up to ~3x the expected tile population stage in shared
+  // memory; larger ones (clusters) in HBM
+  c->np_smem = (uint32_t)std::min<double>(4096.0, std::max<double>(1024.0, 3.0 * c->tc * density));
   uint32_t cap = default_cap((double)cap_n / (double)C, C);
   // flat rows 0..n-1 must fit in one region array
   cap = std::max<uint32_t>(cap, (uint32_t)((cap_n + C - 1) / C));
   c->cap = cap;
-  c->ovf_cap = (uint32_t)std::min<int64_t>(cap_n, std::max<int64_t>(cap_n / 16, 1 << 16));
-  c->scratch_cap = (uint32_t)std::min<int64_t>(cap_n, std::max<int64_t>(cap_n / 8, 1 << 20));
+  // Clusters: the overflow lists (particles beyond their cell's cap) and the
+  // HBM staging of oversized dense tiles take up to 1/4 and 1/2 of the
+  // particles when HBM allows (1/16 and 1/8 at least); a cluster beyond that
+  // fails loudly with MPCD_ERR_CAPACITY.
+  {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double regions = 2.0 * (double)C * cap * 64.0;
+    const double spare = (double)free_b - regions - 4.0 * (1ull << 30);
+    int shift = 2;  // n / 4 overflow entries, n / 2 staged rows
+    // per particle of overflow capacity: 2 lists x (64 B record + 4 B cell) +
+    // 4 B bucket index; of staging: 40 B
+    while (shift < 4 && spare < (double)cap_n * (140.0 / (1 << shift) + 40.0 / (2 << shift)))
+      ++shift;
+    c->ovf_cap = (uint32_t)std::min<int64_t>(cap_n, std::max<int64_t>(cap_n >> shift, 1 << 16));
+    c->scratch_cap =
+        (uint32_t)std::min<int64_t>(cap_n, std::max<int64_t>(cap_n >> (shift - 1), 1 << 20));
+    // densities where a typical tile exceeds the shared-memory staging
+    // (hundreds of particles per cell): every tile may stage in HBM
+    if (c->tc * density >= 0.5 * c->np_smem) c->scratch_cap = (uint32_t)cap_n;
+  }
   auto cleanup = [&](int rc) {
     mpcd_ctx_destroy(c);
     return rc;
@@ -901,17 +951,21 @@ int mpcd_ctx_create(const mpcd_config* cfg, mpcd_ctx** out) {
     c->ovf[b] = carve(c->ovf_slab[b], c->ovf_cap);
     cudaMemset(c->count[b], 0, sizeof(uint32_t) * C);
   }
-  if (cudaMalloc(&c->small, sizeof(uint32_t) * 8) != cudaSuccess ||
+  if (cudaMalloc(&c->small, sizeof(uint32_t) * kSmallWords) != cudaSuccess ||
       cudaMalloc(&c->dense, sizeof(uint32_t) * c->ntiles) != cudaSuccess ||
+      cudaMalloc(&c->dense_bits, sizeof(uint32_t) * ((c->ntiles + 31) / 32)) != cudaSuccess ||
+      cudaMalloc(&c->cell_aux, sizeof(uint32_t) * C) != cudaSuccess ||
+      cudaMalloc(&c->ovf_sorted, sizeof(uint32_t) * c->ovf_cap) != cudaSuccess ||
       cudaMalloc(&c->scratch_id, sizeof(uint32_t) * c->scratch_cap) != cudaSuccess ||
       cudaMalloc(&c->scratch_src, sizeof(uint32_t) * c->scratch_cap) != cudaSuccess ||
       cudaMalloc(&c->scratch_val, sizeof(double) * 4 * c->scratch_cap) != cudaSuccess ||
-      cudaMalloc(&c->partials, sizeof(double) * 8 * (c->ntiles + kDenseGrid)) != cudaSuccess ||
+      cudaMalloc(&c->partials, sizeof(double) * 8 * (c->ntiles + kMainRows)) != cudaSuccess ||
       cudaMalloc(&c->level1, sizeof(double) * kDiagCols * kDiagBlocks) != cudaSuccess ||
       cudaMalloc(&c->diag, sizeof(double) * 16) != cudaSuccess ||
       cudaMalloc(&c->drift_bits, sizeof(unsigned long long)) != cudaSuccess)
     return cleanup(fail(MPCD_ERR_CUDA, "cudaMalloc of per-tile arrays failed"));
-  cudaMemset(c->small, 0, sizeof(uint32_t) * 8);
+  cudaMemset(c->small, 0, sizeof(uint32_t) * kSmallWords);
+  cudaMemset(c->dense_bits, 0, sizeof(uint32_t) * ((c->ntiles + 31) / 32));
   cudaMemset(c->diag, 0, sizeof(double) * 16);
   cudaMemset(c->drift_bits, 0, sizeof(unsigned long long));
   int rc = c->scan.init(C);
@@ -932,7 +986,8 @@ int mpcd_ctx_destroy(mpcd_ctx* c) {
     if (c->ovf_slab[b]) cudaFree(c->ovf_slab[b]);
     if (c->ovf_cell[b]) cudaFree(c->ovf_cell[b]);
   }
-  void* ptrs[] = {c->small, c->dense, c->scratch_id, c->scratch_src, c->scratch_val,
+  void* ptrs[] = {c->small, c->dense, c->dense_bits, c->cell_aux, c->ovf_sorted,
+                  c->scratch_id, c->scratch_src, c->scratch_val,
                   c->partials, c->level1, c->diag, c->com_cap, c->drift_bits};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -956,6 +1011,7 @@ int64_t mpcd_count(const mpcd_ctx* c) {
 }
 int64_t mpcd_current_step(const mpcd_ctx* c) { return c ? c->cur_step : -1; }
 int64_t mpcd_cell_capacity(const mpcd_ctx* c) { return c ? (int64_t)c->cap : -1; }
+int32_t mpcd_tile_cells(const mpcd_ctx* c) { return c ? (int32_t)c->tc : -1; }
 
 int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double* mass,
                 const int64_t* ids, int64_t n, int64_t step, void* stream) {
@@ -968,6 +1024,10 @@ int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double*
   if (n > 0 && !c->cfg.uniform_mass && !mass) return fail(MPCD_ERR_CONFIG, "masses required");
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
+  if (ids && n > 0) {
+    int rc = validate_ids(ids, n, !c->multi);
+    if (rc) return rc;
+  }
   // retire whatever is resident
   for (int b = 0; b < 2; ++b) {
     MPCD_CUDA(cudaMemsetAsync(c->count[b], 0, sizeof(uint32_t) * c->C, st));
@@ -1017,6 +1077,7 @@ int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double*
   c->flat = -1;
   c->cur_step = step;
   c->have_diag = false;
+  c->poisoned = false;
   return check_flags(c, st);
 }
 
@@ -1048,7 +1109,8 @@ int mpcd_run(mpcd_ctx* c, int64_t first_step, int64_t n_steps, int32_t flags, vo
     int rc = launch_step(c, first_step + k, flags, false, as_stream(stream));
     if (rc) return rc;
   }
-  return MPCD_OK;
+  // capacity / RNG failures of any step of the run surface here (one sync)
+  return n_steps > 0 ? check_flags(c, as_stream(stream)) : MPCD_OK;
 }
 
 int mpcd_read_diag(mpcd_ctx* c, mpcd_diag* out, void* stream) {
@@ -1143,19 +1205,21 @@ int mpcd_read_binning(mpcd_ctx* c, int64_t* cells, int64_t* bin_count, int64_t* 
   return MPCD_OK;
 }
 
-int mpcd_step_host(mpcd_ctx* c, double* pos, double* vel, const double* mass, int64_t n,
-                   int64_t step, int32_t flags, double* drift, void* stream) {
+int mpcd_step_rows(mpcd_ctx* c, const double* pos_in, const double* vel_in, const double* mass,
+                   int64_t n, int64_t step, int32_t flags, double* pos_out, double* vel_out,
+                   double* drift, void* stream) {
   clear_error();
   if (!c) return fail(MPCD_ERR_CONFIG, "null context");
   if (c->multi) return fail(MPCD_ERR_CONFIG, "step_host is for a whole-box context");
-  int rc = mpcd_upload(c, pos, vel, mass, nullptr, n, step, stream);
+  if (n > 0 && (!pos_out || !vel_out)) return fail(MPCD_ERR_CONFIG, "output rows required");
+  int rc = mpcd_upload(c, pos_in, vel_in, mass, nullptr, n, step, stream);
   if (rc) return rc;
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
   rc = launch_step(c, step, flags, true, st);
   if (rc) return rc;
-  double* zpos = mapped(pos);
-  double* zvel = mapped(vel);
+  double* zpos = mapped(pos_out);
+  double* zvel = mapped(vel_out);
   if (n > 0 && zpos && zvel) {  // by-id rows straight into the caller's pinned buffers
     k_flat_to_rows_chunked<<<grid_for(n, kRowBlock), kRowBlock, 0, st>>>(c->reg[c->flat], n,
                                                                          zpos, zvel);
@@ -1166,8 +1230,9 @@ int mpcd_step_host(mpcd_ctx* c, double* pos, double* vel, const double* mass, in
     k_flat_to_rows_chunked<<<grid_for(n, kRowBlock), kRowBlock, 0, st>>>(c->reg[c->flat], n, tmp,
                                                                          tmp + 3 * n);
     MPCD_LAUNCH_CHECK();
-    MPCD_CUDA(cudaMemcpyAsync(pos, tmp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
-    MPCD_CUDA(cudaMemcpyAsync(vel, tmp + 3 * n, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+    MPCD_CUDA(cudaMemcpyAsync(pos_out, tmp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, st));
+    MPCD_CUDA(cudaMemcpyAsync(vel_out, tmp + 3 * n, sizeof(double) * 3 * n,
+                              cudaMemcpyDeviceToHost, st));
     MPCD_CUDA(cudaFreeAsync(tmp, st));
   }
   mpcd_diag d;
@@ -1175,6 +1240,36 @@ int mpcd_step_host(mpcd_ctx* c, double* pos, double* vel, const double* mass, in
   if (rc) return rc;
   if (drift) *drift = d.max_cell_drift;
   return MPCD_OK;
+}
+
+int mpcd_step_host(mpcd_ctx* c, double* pos, double* vel, const double* mass, int64_t n,
+                   int64_t step, int32_t flags, double* drift, void* stream) {
+  return mpcd_step_rows(c, pos, vel, mass, n, step, flags, pos, vel, drift, stream);
+}
+
+int mpcd_host_alloc(int64_t bytes, void** out) {
+  clear_error();
+  if (!out || bytes < 0) return fail(MPCD_ERR_CONFIG, "bad argument");
+  *out = nullptr;
+  if (bytes == 0) return MPCD_OK;
+  MPCD_CUDA(cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  return MPCD_OK;
+}
+
+int mpcd_host_free(void* ptr) {
+  clear_error();
+  if (ptr) MPCD_CUDA(cudaFreeHost(ptr));
+  return MPCD_OK;
+}
+
+int mpcd_host_is_pinned(const void* ptr) {
+  if (!ptr) return 0;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return a.type == cudaMemoryTypeHost ? 1 : 0;
 }
 
 int mpcd_init_device(mpcd_ctx* c, int64_t n, double velocity_variance, int64_t step, void* stream) {
@@ -1216,6 +1311,7 @@ int mpcd_init_device(mpcd_ctx* c, int64_t n, double velocity_variance, int64_t s
   c->flat = -1;
   c->cur_step = step;
   c->have_diag = false;
+  c->poisoned = false;
   return check_flags(c, st);
 }
 
@@ -1436,18 +1532,3 @@ void mpcd_grid_shift(int32_t prng, uint64_t seed, uint64_t step, double cell_siz
 }
 
 }  // extern "C"
-
-#ifdef MPCD_TIMING
-// Tuning builds only (-DMPCD_TIMING): per-phase clock64 sums of the k_step
-// consumer warps (tools/phase_timing.py).
-extern "C" int mpcd_debug_phase_cycles(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, mpcd::g_phase_cycles, sizeof(unsigned long long) * 10) !=
-      cudaSuccess)
-    return MPCD_ERR_CUDA;
-  if (reset) {
-    unsigned long long z[10] = {0};
-    cudaMemcpyToSymbol(mpcd::g_phase_cycles, z, sizeof(z));
-  }
-  return MPCD_OK;
-}
-#endif

@@ -1,5 +1,6 @@
 // mpcd_step.cuh -- the one-kernel SRD step over fixed-capacity cell regions
-// (included once, by mpcd_engine.cu).
+// (included by mpcd_engine.cu, which launches the non-template kernels, and by
+// the four mpcd_step_<mode>.cu units, which instantiate the step variants).
 //
 // Layout: every collision cell c of the step's grid owns
 // `cap` record slots [c*cap, (c+1)*cap) of each record array; count[c] says
@@ -85,7 +86,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// SYS: system scope, for the words that other GPUs claim in too (fused
+// migration: a peer's k_step adds to this domain's counts over NVLink, and
+// device-scope atomics of two GPUs are not atomic with respect to each other)
+template <bool SYS = false>
 __device__ __forceinline__ uint32_t count_claim(uint32_t* p, uint32_t v) {
+  if (SYS) return atomicAdd_system(p, v);
   if (!MPCD_CNT_EVICT_LAST) return atomicAdd(p, v);
   uint32_t old;
   asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], %2, %3;"
@@ -157,12 +163,20 @@ struct StepArgs {
   double* partials;           // per tile: px py pz sum(m v^2) mass
   double* com_cap;            // COM: per cell com[3], count
   unsigned long long* drift_bits;
-  uint32_t* flags;            // [0] dense tiles, [1] rng failure, [2] overflow list full
-  uint32_t* dense;            // dense tile list
-  uint32_t* scratch_n;        // dense-kernel staging allocator
-  uint32_t* scratch_id;       // dense-kernel staging (n entries)
-  double* scratch_val;        // dense-kernel staging (4 n doubles)
+  // [0] dense tiles, [1] rng failure, [2] overflow list full, [3] routing
+  // error, [8] overflow bucket allocator, [9] dense staging exhausted
+  uint32_t* flags;
+  uint32_t* dense;            // dense tile list (arrival order)
+  uint32_t* dense_bits;       // one bit per tile: queued for k_step_dense
+  uint32_t* cell_aux;         // per cell: its overflow bucket in ovf_sorted
+  uint32_t* ovf_sorted;       // overflow entries bucketed by cell
+  uint32_t* scratch_n;        // dense-kernel staging allocator (tiles above np_smem)
+  uint32_t* scratch_id;       // dense-kernel staging (scratch_cap entries)
+  double* scratch_val;        // dense-kernel staging (4 scratch_cap doubles)
   uint32_t* scratch_src;      // dense-kernel: source slot of each staged row
+  uint32_t scratch_cap;
+  uint32_t np_smem;           // particles of a dense tile staged in shared memory
+  int tc, cw;                 // cells per tile, cells per consumer warp (tc / 4)
   int L0, L1, L2;
   int64_t C;
   double a, dt, cs, sn, box0, box1, box2;
@@ -171,7 +185,7 @@ struct StepArgs {
   uint64_t axis_prefix;       // key_prefix(seed, step, AXIS)
   int prng;
   double m0;
-  int64_t part_base;          // first partials row of the dense kernel's CTAs
+  int64_t dense_row0;         // partials row of dense tile t: dense_row0 + t
   // multi-domain (MODE == kMulti): this context owns the cells [o, o + L) of
   // a global G0 x G1 x G2 grid split into uniform blocks; rank of a block =
   // (bx * R1 + by) * R2 + bz.  Leavers go to send[dest * send_cap + slot].
@@ -203,7 +217,7 @@ __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c)
 }
 
 #ifndef MPCD_TC
-#define MPCD_TC 16
+#define MPCD_TC 32
 #endif
 #ifndef MPCD_MAXPT
 #define MPCD_MAXPT 256
@@ -211,14 +225,14 @@ __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c)
 #ifndef MPCD_MINB
 #define MPCD_MINB 4
 #endif
-constexpr int kTC = MPCD_TC;    // cells per tile (one producer lane per cell, <= 32)
+constexpr int kTC = MPCD_TC;    // most cells per tile (one producer lane per cell, <= 32)
 constexpr int kNT = 256;        // threads of the dense-tile CTA
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
 constexpr int kPadBit = 0x80;  // slot-table flag of a padding slot
 constexpr int kDiagCols = 7;  // partial columns: px py pz sum(m v^2) mass collided migrated
 
 // ------------------------------------------------------------ cell index --
-__device__ __noinline__ int cell_coord_slow(double t, int L) {
+static __device__ __noinline__ int cell_coord_slow(double t, int L) {
   return (int)pymod(__double2ll_rd(t), (int64_t)L);
 }
 
@@ -244,7 +258,7 @@ __device__ __forceinline__ uint32_t next_cell(const StepArgs& A, double x, doubl
 // A leaver's owner and its cell in the owner's numbering (uniform blocks:
 // global mod block), packed (dest << 32 | key).  Out of line: the divisions
 // are rare and would otherwise bloat every inlined copy of the hot loop.
-__device__ __noinline__ uint64_t foreign_target(int gx, int gy, int gz, int L0, int L1, int L2,
+static __device__ __noinline__ uint64_t foreign_target(int gx, int gy, int gz, int L0, int L1, int L2,
                                                 int R1, int R2) {
   const int dest = ((gx / L0) * R1 + gy / L1) * R2 + gz / L2;
   const uint32_t key = ((uint32_t)(gx % L0) * (uint32_t)L1 + (uint32_t)(gy % L1)) * (uint32_t)L2 +
@@ -255,12 +269,12 @@ __device__ __noinline__ uint64_t foreign_target(int gx, int gy, int gz, int L0, 
 // Fused migration of one leaver: claim a slot in its owner's next-step cell
 // and store it there over peer memory (or the owner's overflow list).  Out
 // of line, scalar arguments only (no address of the kernel's parameters).
-__device__ __noinline__ void fused_put(const PeerBufs* peers, int b, uint32_t cap,
+static __device__ __noinline__ void fused_put(const PeerBufs* peers, int b, uint32_t cap,
                                        uint32_t ovf_cap, int dest, uint32_t key, double x,
                                        double y, double z, uint32_t id, double vx, double vy,
                                        double vz, double m) {
   const PeerBufs& P = peers[dest];
-  const uint32_t slot = atomicAdd(&P.count[b][key], 1u);
+  const uint32_t slot = atomicAdd_system(&P.count[b][key], 1u);
   // two 16-byte stores per record here: ptxas mis-assembles the 256-bit
   // inline-asm store inside a called (non-inlined) function
   auto put = [&](const Recs& r, uint64_t dst) {
@@ -272,12 +286,12 @@ __device__ __noinline__ void fused_put(const PeerBufs* peers, int b, uint32_t ca
   if (slot < cap) {
     put(P.reg[b], (uint64_t)key * cap + slot);
   } else {  // the owner's cell is full: its overflow list
-    const uint32_t q = atomicAdd(&P.small[4 + b], 1u);
+    const uint32_t q = atomicAdd_system(&P.small[4 + b], 1u);
     if (q < ovf_cap) {
       put(P.ovf[b], q);
       P.ovf_cell[b][q] = key;
     } else {
-      atomicOr(&P.small[2], 1u);
+      atomicOr_system(&P.small[2], 1u);
     }
   }
 }
@@ -302,7 +316,7 @@ __device__ __forceinline__ bool next_cell_multi(const StepArgs& A, double x, dou
   return false;
 }
 
-__device__ __noinline__ double wrap_slow(double x, double box) { return wrap(x, box); }
+static __device__ __noinline__ double wrap_slow(double x, double box) { return wrap(x, box); }
 
 // particles.py:52-67 fast path (positions move less than a box per step)
 __device__ __forceinline__ double wrap_fast(double x, double box) {
@@ -388,23 +402,25 @@ __device__ __forceinline__ double cell_drift(const double* pre, const double* po
 #ifndef MPCD_NOAGG
 #define MPCD_NOAGG 1
 #endif
+template <bool SYS>
 __device__ __forceinline__ void claim_slot(const StepArgs& A, bool active, uint32_t key,
                                            unsigned& grp, uint32_t& base) {
   grp = 0u;
   base = 0u;
   if (MPCD_NOAGG) {  // one atomic per particle: the slot itself
-    if (active) base = count_claim(&A.count_out[key], 1u);
+    if (active) base = count_claim<SYS>(&A.count_out[key], 1u);
     return;
   }
   const unsigned act = __ballot_sync(0xffffffffu, active);
   if (active) {
     grp = __match_any_sync(act, key);
     if ((int)(threadIdx.x & 31) == __ffs(grp) - 1)
-      base = atomicAdd(&A.count_out[key], (uint32_t)__popc(grp));
+      base = count_claim<SYS>(&A.count_out[key], (uint32_t)__popc(grp));
   }
 }
 
 // Store one collided particle into its claimed slot (or the overflow list).
+template <bool SYS>
 __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, unsigned grp,
                                             uint32_t base, const double* o, uint32_t id,
                                             double m) {
@@ -417,10 +433,12 @@ __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, uns
   if (slot < A.cap) {
     store_rec(A.out, (uint64_t)key * A.cap + slot, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
   } else {  // full cell: overflow list (gathered by the dense kernel next step)
-    const uint32_t q = atomicAdd(A.ovf_n_out, 1u);
+    const uint32_t q = SYS ? atomicAdd_system(A.ovf_n_out, 1u) : atomicAdd(A.ovf_n_out, 1u);
     if (q < A.ovf_cap) {
       store_rec(A.ovf_out, q, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
       A.ovf_cell_out[q] = key;
+    } else if (SYS) {
+      atomicOr_system(&A.flags[2], 1u);
     } else {
       atomicOr(&A.flags[2], 1u);
     }
@@ -481,8 +499,8 @@ __device__ __forceinline__ void emit(const StepArgs& A, bool active, double nx, 
   }
   unsigned grp;
   uint32_t base;
-  claim_slot(A, local, key, grp, base);
-  if (local) finish_slot(A, key, grp, base, o, id, m);
+  claim_slot<MODE == kFused>(A, local, key, grp, base);
+  if (local) finish_slot<MODE == kFused>(A, key, grp, base, o, id, m);
 }
 
 // ----------------------------------------------- shared-memory row access --
@@ -544,8 +562,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 #ifdef MPCD_TIMING
-__device__ unsigned long long g_phase_cycles[10];
-__device__ unsigned long long g_wait_cycles;
+static __device__ unsigned long long g_phase_cycles[10];
 // per-warp shared accumulators (S.tim), flushed once per warp at kernel end
 #define MPCD_PROBE(k)                                                              \
   do {                                                                             \
@@ -564,7 +581,7 @@ __device__ unsigned long long g_wait_cycles;
 // counts, lays out its records in shared memory (each cell padded to a
 // multiple of 4 slots), writes the slot -> cell table, issues one
 // cp.async.bulk (TMA) per cell and record array, zeroes the consumed counts
-// and draws the cells' rotation axes.  Each consumer warp owns kCW = 4 cells
+// and draws the cells' rotation axes.  Each consumer warp owns A.cw <= kCW = 8 cells
 // of the tile and runs every phase on them alone -- rank, moments, com,
 // rotation, stream, next-cell claims and stores -- synchronised only by
 // __syncwarp, in warp-private shared scratch; so consumer warps never wait
@@ -572,7 +589,7 @@ __device__ unsigned long long g_wait_cycles;
 // counts one arrival per consumer warp).
 constexpr int kMaxPT = MPCD_MAXPT;     // padded record slots per tile in shared memory
 #ifndef MPCD_CW
-#define MPCD_CW 4
+#define MPCD_CW 8
 #endif
 constexpr int kCW = MPCD_CW;           // cells per consumer warp
 constexpr int kNCW = kTC / kCW;        // consumer warps
@@ -629,22 +646,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Tile geometry: FIX = 16 compiles the 16-cell tile of ~10 particles per
+// cell (the common density) into the kernel; FIX = 0 reads A.tc / A.cw (any
+// multiple of kNCW up to kTC).  The compile-time form is ~1.5 % faster.
+#define TILE_CELLS(A) (FIX ? FIX : (A).tc)
+#define WARP_CELLS(A) (FIX ? FIX / kNCW : (A).cw)
+
+template <int FIX>
 __device__ __forceinline__ uint32_t tile_count(const StepArgs& A, int64_t tl, int64_t ntiles) {
   const int lane = threadIdx.x & 31;
-  const int64_t c = tl * kTC + lane;
-  return (lane < kTC && tl < ntiles && c < A.C) ? __ldcg(A.count_in + c) : 0u;
+  const int64_t c = tl * TILE_CELLS(A) + lane;
+  return (lane < TILE_CELLS(A) && tl < ntiles && c < A.C) ? __ldcg(A.count_in + c) : 0u;
 }
 
 // Producer warp: lay out tile `tl` in `B` from its counts (one per lane),
 // start its copies, draw its axes.  Completes two arrivals on `full` (one
 // with the byte count, one once the generic writes are done).
-template <int MODE>
+template <int MODE, int FIX>
 __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint64_t* full,
                                              int64_t tl, int64_t ntiles, uint32_t cnt,
                                              uint64_t pol) {
   const int lane = threadIdx.x & 31;
-  const int64_t c0 = tl * kTC;
-  const int nc = tl < ntiles ? (int)min((int64_t)kTC, A.C - c0) : 0;
+  const int64_t c0 = tl * TILE_CELLS(A);
+  const int nc = tl < ntiles ? (int)min((int64_t)TILE_CELLS(A), A.C - c0) : 0;
   const uint32_t k = min(cnt, A.cap);
   const uint32_t pad = (k + 3u) & ~3u;
   uint32_t incl = pad;
@@ -665,7 +689,10 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane == 0) {
     B.off[0] = 0;
     B.skip = skip ? 1 : 0;
-    if (skip && tl < ntiles) A.dense[atomicAdd(&A.flags[0], 1u)] = (uint32_t)tl;
+    if (skip && tl < ntiles) {  // queued for k_step_dense
+      A.dense[atomicAdd(&A.flags[0], 1u)] = (uint32_t)tl;
+      atomicOr(&A.dense_bits[tl >> 5], 1u << (tl & 31));
+    }
   }
   if (skip) {
     __syncwarp();
@@ -857,7 +884,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       // the staging below and the next row's whole chain
       grp[r] = 0u;
       base[r] = 0u;
-      if (!BYID && j0 + 32 * r < j1) claim_slot(A, stay[r], key[r], grp[r], base[r]);
+      if (!BYID && j0 + 32 * r < j1)
+        claim_slot<MODE == kFused>(A, stay[r], key[r], grp[r], base[r]);
 #endif
       const double m = mm[r];
       const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
@@ -894,7 +922,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       grp[r] = 0u;
       base[r] = 0u;
       if (j0 + 32 * r < j1)  // warp-uniform: every lane takes part in the ballot
-        claim_slot(A, stay[r], key[r], grp[r], base[r]);
+        claim_slot<MODE == kFused>(A, stay[r], key[r], grp[r], base[r]);
     }
   }
   __syncwarp();
@@ -926,7 +954,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   if (!BYID) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (stay[r]) finish_slot(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
+      if (stay[r]) finish_slot<MODE == kFused>(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
   }
   if (decomposed(MODE) && __any_sync(0xffffffffu, leavers != 0u)) {
     // the pass's leavers, from their parked slots: one copy of the sending
@@ -972,7 +1000,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   MPCD_PROBE(7);
 }
 
-template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
+template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE, int FIX>
 __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int64_t ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
@@ -996,12 +1024,12 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     // by 0.1 %; evict-unchanged is the same
     const uint64_t pol = policy_evict_normal();
     int64_t tile = blockIdx.x;
-    uint32_t cnt = tile_count(A, tile, ntiles);
+    uint32_t cnt = tile_count<FIX>(A, tile, ntiles);
     for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
       const int b = (int)(i % kStages);
-      const uint32_t cnt_next = tile_count(A, tile + G, ntiles);  // in flight meanwhile
+      const uint32_t cnt_next = tile_count<FIX>(A, tile + G, ntiles);  // in flight meanwhile
       if (i >= kStages) mbar_wait(&S.empty[b], (uint32_t)((i / kStages) - 1) & 1u);
-      prepare_tile<MODE>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
+      prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
       cnt = cnt_next;
     }
     return;
@@ -1009,7 +1037,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 
   // ------------------------------------------------------------ consumers
   WarpScratch& W = S.w[warp];
-  const int cw0 = warp * kCW;  // this warp's first cell of every tile
+  const int cw0 = warp * WARP_CELLS(A);  // this warp's first cell of every tile
   // px py pz sum(m v^2) mass, particles collided, particles sent to other ranks
   double acc[kDiagCols] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int64_t tile = blockIdx.x;
@@ -1024,8 +1052,8 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     if (lane == 0) S.tim[warp][8] += (unsigned long long)(clock64() - tw0);
     if (lane == 0) S.tim[warp][9] += 1ull;
 #endif
-    const int64_t c0 = tile * kTC;
-    const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)kCW, A.C - c0 - cw0));
+    const int64_t c0 = tile * TILE_CELLS(A);
+    const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)WARP_CELLS(A), A.C - c0 - cw0));
     if (ncw == 0) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[b]);
@@ -1071,29 +1099,91 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 }
 
 // ----------------------------------------------------- dense-tile kernel --
-// Tiles with a cell above `cap` or more than kMaxPT padded rows.  Gathers each
-// cell's region slots plus its overflow entries into HBM staging, then the
-// same phases with plain loops; ranking is O(k^2) per cell.  One CTA per
-// queued tile (grid-strided); staging ranges come from a bump allocator.
+// Tiles that k_step cannot stage: a cell above `cap` (its extra particles sit
+// in the overflow list), a cell of more than kSlotsW padded rows, or more than
+// kMaxPT padded rows in the tile.  These are rare at the density a context's
+// tile size was chosen for (mpcd_ctx_create); this is the general path for
+// clusters and for densities above ~40 particles per cell.  Work is O(n)
+// apart from the in-cell ranking (O(k^2 / threads) per cell of k particles):
+//
+//   k_dense_prep   per queued tile, reserve each overflowing cell's bucket in
+//                  ovf_sorted (cell_aux[c] = its first position);
+//   k_ovf_bucket   each overflow entry into its cell's bucket;
+//   k_step_dense   one CTA per queued tile: gather the tile's particles (region
+//                  slots + bucket) into shared memory (or, above np_smem, into
+//                  HBM staging from a bounded allocator), rank by id, the same
+//                  phases as k_step, one partials row per tile.
+//
+// Every overflow entry belongs to a queued tile: a cell above cap makes its
+// tile dense.  Results never depend on the (arrival) order of the queue: the
+// diagnostics rows are per tile and reduced in tile order (k_diag_partial).
+#ifndef MPCD_STEP_VARIANTS_ONLY
+__global__ void __launch_bounds__(256) k_dense_prep(const StepArgs A) {
+  const uint32_t n_dense = *(volatile uint32_t*)&A.flags[0];
+  const uint32_t n_ovf = min(*(volatile uint32_t*)A.ovf_n_in, A.ovf_cap);
+  if (n_ovf == 0) return;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n_dense;
+       e += gridDim.x * blockDim.x) {
+    const int64_t c0 = (int64_t)A.dense[e] * A.tc;
+    const int nc = (int)min((int64_t)A.tc, A.C - c0);
+    uint32_t tot = 0;
+    for (int lc = 0; lc < nc; ++lc) {
+      const uint32_t cnt = A.count_in[c0 + lc];
+      tot += cnt > A.cap ? cnt - A.cap : 0u;
+    }
+    if (!tot) continue;
+    uint32_t base = atomicAdd(&A.flags[8], tot);
+    for (int lc = 0; lc < nc; ++lc) {
+      const uint32_t cnt = A.count_in[c0 + lc];
+      if (cnt > A.cap) {
+        A.cell_aux[c0 + lc] = base;
+        base += cnt - A.cap;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ovf_bucket(const StepArgs A) {
+  if (*(volatile uint32_t*)&A.flags[0] == 0u) return;
+  const uint32_t n_ovf = min(*(volatile uint32_t*)A.ovf_n_in, A.ovf_cap);
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n_ovf; o += gridDim.x * blockDim.x) {
+    const uint32_t c = A.ovf_cell_in[o];
+    if ((int64_t)c >= A.C) continue;
+    const uint32_t pos = atomicAdd(&A.cell_aux[c], 1u);
+    if (pos < A.ovf_cap) A.ovf_sorted[pos] = o;
+  }
+}
+
+#endif  // MPCD_STEP_VARIANTS_ONLY
+
+// Bytes of dynamic shared memory k_step_dense stages `np` particles in.
+__host__ __device__ constexpr size_t dense_smem_bytes(uint32_t np) {
+  return (size_t)np * (4 * sizeof(double) + 2 * sizeof(uint32_t));
+}
+
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
 __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* const sm_val = reinterpret_cast<double*>(dsm);
+  uint32_t* const sm_id = reinterpret_cast<uint32_t*>(sm_val + 4 * (size_t)A.np_smem);
+  uint32_t* const sm_src = sm_id + A.np_smem;
   __shared__ uint32_t s_cnt[kTC];
   __shared__ uint32_t s_off[kTC + 1];
-  __shared__ uint32_t s_fill[kTC];
+  __shared__ uint32_t s_nreg[kTC];
+  __shared__ uint32_t s_obeg[kTC];
   __shared__ uint32_t s_base;
+  __shared__ int s_mode;  // 0 shared-memory staging, 1 HBM staging, -1 no room
   __shared__ double s_mom[kTC * 4];
   __shared__ double s_post[kTC * 4];
   __shared__ double s_cx[kTC * 6];
+  __shared__ double s_mig[kNT / 32];
   const int t = threadIdx.x;
   const uint32_t n_dense = *(volatile uint32_t*)&A.flags[0];
   const uint32_t n_ovf = min(*(volatile uint32_t*)A.ovf_n_in, A.ovf_cap);
-  double dacc = 0.0;  // thread t < kDiagCols: this CTA's partial sum of column t
-  double dmig = 0.0;  // this thread's particles sent to other ranks
-  __shared__ double s_mig[kNT / 32];
   for (uint32_t e = blockIdx.x; e < n_dense; e += gridDim.x) {
-    const int64_t tile = A.dense[e];  // sorted by k_sort_dense: deterministic sums
-    const int64_t c0 = tile * kTC;
-    const int nc = (int)min((int64_t)kTC, A.C - c0);
+    const int64_t tile = A.dense[e];
+    const int64_t c0 = tile * A.tc;
+    const int nc = (int)min((int64_t)A.tc, A.C - c0);
     __syncthreads();
     if (t == 0) {
       uint32_t acc = 0;
@@ -1101,30 +1191,52 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
         const uint32_t cnt = lc < nc ? A.count_in[c0 + lc] : 0u;
         s_cnt[lc] = cnt;
         s_off[lc] = acc;
-        s_fill[lc] = min(cnt, A.cap);
+        s_nreg[lc] = min(cnt, A.cap);
+        // bucket end (k_ovf_bucket advanced it) minus this cell's entries
+        s_obeg[lc] = cnt > A.cap ? A.cell_aux[c0 + lc] - (cnt - A.cap) : 0u;
         acc += cnt;
       }
       s_off[kTC] = acc;
-      s_base = atomicAdd(A.scratch_n, acc);
+      s_mode = 0;
+      s_base = 0;
+      if (acc > A.np_smem) {
+        const uint32_t b = atomicAdd(A.scratch_n, acc);
+        if ((uint64_t)b + acc <= (uint64_t)A.scratch_cap) {
+          s_mode = 1;
+          s_base = b;
+        } else {
+          s_mode = -1;
+          atomicOr(&A.flags[9], 1u);  // MPCD_ERR_CAPACITY: the particles are lost
+        }
+      }
     }
     __syncthreads();
     const uint32_t np = s_off[kTC];
-    uint32_t* g_id = A.scratch_id + s_base;
-    uint32_t* g_src = A.scratch_src + s_base;  // region slot, or 0x80000000|overflow index
-    double* g_val = A.scratch_val + 4 * (uint64_t)s_base;
-    // gather: region slots in order, then overflow entries (claimed in order)
-    for (int lc = 0; lc < nc; ++lc)
-      for (uint32_t s = t; s < min(s_cnt[lc], A.cap); s += kNT) {
-        g_id[s_off[lc] + s] = A.in.p[(uint64_t)(c0 + lc) * A.cap + s].id;
-        g_src[s_off[lc] + s] = s;
-      }
-    for (uint32_t o = t; o < n_ovf; o += kNT) {
-      const uint32_t c = A.ovf_cell_in[o];
-      if (c >= (uint64_t)c0 && c < (uint64_t)(c0 + nc)) {
-        const int lc = (int)(c - c0);
-        const uint32_t at = s_off[lc] + atomicAdd(&s_fill[lc], 1u);
-        g_id[at] = A.ovf_in.p[o].id;
-        g_src[at] = 0x80000000u | o;
+    if (s_mode < 0) {
+      if (t < nc) A.count_in[c0 + t] = 0u;
+      continue;
+    }
+    uint32_t* const g_id = s_mode ? A.scratch_id + s_base : sm_id;
+    uint32_t* const g_src = s_mode ? A.scratch_src + s_base : sm_src;  // slot, or 0x80000000|entry
+    double* const g_val = s_mode ? A.scratch_val + 4 * (uint64_t)s_base : sm_val;
+    // gather: region slots, then the cell's overflow bucket
+    for (int lc = 0; lc < nc; ++lc) {
+      const uint32_t nreg = s_nreg[lc], nall = s_cnt[lc];
+      for (uint32_t s = t; s < nall; s += kNT) {
+        uint32_t id = kSentinel, src = 0x80000000u;
+        if (s < nreg) {
+          id = A.in.p[(uint64_t)(c0 + lc) * A.cap + s].id;
+          src = s;
+        } else {
+          const uint32_t pos = s_obeg[lc] + (s - nreg);
+          const uint32_t o = pos < A.ovf_cap ? A.ovf_sorted[pos] : 0xFFFFFFFFu;
+          if (o < n_ovf) {  // (else: entries were dropped, flags[2] already set)
+            id = A.ovf_in.p[o].id;
+            src = 0x80000000u | o;
+          }
+        }
+        g_id[s_off[lc] + s] = id;
+        g_src[s_off[lc] + s] = src;
       }
     }
     __syncthreads();
@@ -1138,19 +1250,22 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
     };
     auto rec_p = [&](uint32_t j, int lc) -> const PRec& {
       const uint32_t s = g_src[j];
-      return (s & 0x80000000u) ? A.ovf_in.p[s & 0x7FFFFFFFu] : A.in.p[(uint64_t)(c0 + lc) * A.cap + s];
+      return (s & 0x80000000u) ? A.ovf_in.p[min(s & 0x7FFFFFFFu, A.ovf_cap - 1u)]
+                               : A.in.p[(uint64_t)(c0 + lc) * A.cap + s];
     };
     auto rec_v = [&](uint32_t j, int lc) -> const VRec& {
       const uint32_t s = g_src[j];
-      return (s & 0x80000000u) ? A.ovf_in.v[s & 0x7FFFFFFFu] : A.in.v[(uint64_t)(c0 + lc) * A.cap + s];
+      return (s & 0x80000000u) ? A.ovf_in.v[min(s & 0x7FFFFFFFu, A.ovf_cap - 1u)]
+                               : A.in.v[(uint64_t)(c0 + lc) * A.cap + s];
     };
+    // rank by id inside the cell (ids are unique): the stable argsort order
     auto rank_of = [&](uint32_t j, int lc) {
       const uint32_t me = g_id[j];
       uint32_t rank = 0;
       for (uint32_t q = s_off[lc]; q < s_off[lc + 1]; ++q) rank += (g_id[q] < me) ? 1u : 0u;
       return s_off[lc] + rank;
     };
-    // staged rows live after the tile's np ids/srcs in g_val (4 per row)
+    // pre-collision (m v, m) rows in rank order
     for (uint32_t j = t; j < np; j += kNT) {
       const int lc = cell_of(j);
       const uint32_t s = rank_of(j, lc);
@@ -1179,6 +1294,9 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       }
     }
     __syncthreads();
+    // each rank-order row is rewritten with its post-collision row below;
+    // the ranks come from the ids, which stay, so the loop is race-free
+    double dmig = 0.0;
     for (uint32_t base = 0; base < np; base += kNT) {
       const uint32_t j = base + t;
       const bool active = j < np;
@@ -1197,7 +1315,6 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
         nx = wrap(p.x + w[0] * A.dt, A.box0);
         ny = wrap(p.y + w[1] * A.dt, A.box1);
         nz = wrap(p.z + w[2] * A.dt, A.box2);
-        // pre-collision rows of slot s are no longer needed: post rows
         g_val[4 * s] = m * w[0]; g_val[4 * s + 1] = m * w[1]; g_val[4 * s + 2] = m * w[2];
         g_val[4 * s + 3] = m * (((0.0 + w[0] * w[0]) + w[1] * w[1]) + w[2] * w[2]);
       }
@@ -1208,10 +1325,20 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       const int lc = task >> 2, comp = task & 3;
       s_post[task] = s_cnt[lc] ? reduceat(g_val + 4 * (uint64_t)s_off[lc] + comp, (int64_t)s_cnt[lc], 4) : 0.0;
     }
+    for (int o = 16; o > 0; o >>= 1) dmig += __shfl_xor_sync(0xffffffffu, dmig, o);
+    if ((t & 31) == 0) s_mig[t >> 5] = dmig;
     __syncthreads();
-    if (t < 6)
-      for (int lc = 0; lc < nc; ++lc)
-        dacc += (t < 4) ? s_post[lc * 4 + t] : (t == 4 ? s_mom[lc * 4 + 3] : (double)s_cnt[lc]);
+    // this tile's partials row: px py pz sum(m v^2) mass collided migrated
+    if (t < kDiagCols) {
+      double s = 0.0;
+      if (t < 6) {
+        for (int lc = 0; lc < nc; ++lc)
+          s += (t < 4) ? s_post[lc * 4 + t] : (t == 4 ? s_mom[lc * 4 + 3] : (double)s_cnt[lc]);
+      } else {
+        for (int w = 0; w < kNT / 32; ++w) s += s_mig[w];
+      }
+      A.partials[(A.dense_row0 + tile) * 8 + t] = s;
+    }
     if (DRIFT && t >= 32 && t < 64) {
       double worst = 0.0;
       for (int lc = t - 32; lc < nc; lc += 32)
@@ -1222,40 +1349,47 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
     if (t < nc) A.count_in[c0 + t] = 0u;
   }
   if (A.peers) __threadfence_system();
-  for (int o = 16; o > 0; o >>= 1) dmig += __shfl_xor_sync(0xffffffffu, dmig, o);
-  if ((t & 31) == 0) s_mig[t >> 5] = dmig;
-  __syncthreads();
-  if (t == 6)
-    for (int w = 0; w < kNT / 32; ++w) dacc += s_mig[w];
-  if (t < kDiagCols) A.partials[(A.part_base + blockIdx.x) * 8 + t] = dacc;
-}
-
-// The dense-tile list is appended in arbitrary order; sort it (ascending) so
-// that each dense CTA's partial sums run over the same tiles every run.
-__global__ void k_sort_dense(uint32_t* list, const uint32_t* flags) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  const uint32_t n = flags[0];
-  for (uint32_t i = 1; i < n; ++i) {
-    const uint32_t v = list[i];
-    uint32_t j = i;
-    for (; j > 0 && list[j - 1] > v; --j) list[j] = list[j - 1];
-    list[j] = v;
-  }
 }
 
 // ---------------------------------------------------- diagnostics reduce --
 constexpr int kDiagBlocks = 592;
 
-__global__ void __launch_bounds__(256) k_diag_partial(const double* partials, int64_t ntiles,
+#ifndef MPCD_STEP_VARIANTS_ONLY
+// Level 1 of the fixed-order diagnostics reduction: block b sums its share of
+// k_step's per-CTA rows [0, main_rows) and then, when tiles went to the dense
+// kernel, the rows of the queued tiles in its share of the tile range, in
+// tile order (their queue bits are cleared on the way).
+__global__ void __launch_bounds__(256) k_diag_partial(const double* partials, int64_t main_rows,
+                                                     int64_t dense_row0, int64_t ntiles,
+                                                     uint32_t* dense_bits, const uint32_t* flags,
                                                      double* level1) {
   __shared__ double s[kDiagCols][256];
   const int t = threadIdx.x;
-  const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = blockIdx.x * per, hi = min(ntiles, lo + per);
   double acc[kDiagCols] = {0, 0, 0, 0, 0, 0, 0};
-  for (int64_t i = lo + t; i < hi; i += 256)
+  {
+    const int64_t per = (main_rows + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * per, hi = min(main_rows, lo + per);
+    for (int64_t i = lo + t; i < hi; i += 256)
 #pragma unroll
-    for (int c = 0; c < kDiagCols; ++c) acc[c] += partials[i * 8 + c];
+      for (int c = 0; c < kDiagCols; ++c) acc[c] += partials[i * 8 + c];
+  }
+  if (*(volatile const uint32_t*)&flags[0] != 0u) {
+    const int64_t words = (ntiles + 31) / 32;
+    const int64_t per = (words + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * per, hi = min(words, lo + per);
+    for (int64_t w = lo + t; w < hi; w += 256) {
+      uint32_t bits = dense_bits[w];
+      if (!bits) continue;
+      dense_bits[w] = 0u;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const double* row = partials + (dense_row0 + w * 32 + b) * 8;
+#pragma unroll
+        for (int c = 0; c < kDiagCols; ++c) acc[c] += row[c];
+      }
+    }
+  }
 #pragma unroll
   for (int c = 0; c < kDiagCols; ++c) s[c][t] = acc[c];
   __syncthreads();
@@ -1298,7 +1432,10 @@ __global__ void __launch_bounds__(32) k_diag_finalize(const double* level1, int 
     flags[0] = 0u;         // dense-tile list consumed
     *ovf_n_consumed = 0u;  // this step's input overflow list consumed
     *scratch_n = 0u;
+    flags[8] = 0u;  // overflow bucket allocator
   }
 }
+
+#endif  // MPCD_STEP_VARIANTS_ONLY
 
 }  // namespace mpcd

@@ -16,7 +16,7 @@ backends registered in the same backend dispatch (engine.py:524-542):
 from __future__ import annotations
 
 import ctypes as C
-import math
+import warnings
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -24,7 +24,7 @@ import numpy as np
 from . import _dev, _lib
 from .collision import GridShift, sample_grid_shift
 from .errors import ConfigError, MpcdError
-from .params import SimParams
+from .params import SCHEME_MIGRATION, SimParams
 from .particles import ParticleSet, init_system
 
 BACKEND_CUDA = "cuda"
@@ -87,6 +87,15 @@ class EngineContext:
     @property
     def n(self) -> int:
         return int(self._lib.mpcd_count(self.handle))
+
+    @property
+    def tile_cells(self) -> int:
+        """Cells per k_step tile (16, 8 or 4: follows capacity / cells)."""
+        return int(self._lib.mpcd_tile_cells(self.handle))
+
+    @property
+    def cell_capacity(self) -> int:
+        return int(self._lib.mpcd_cell_capacity(self.handle))
 
     def upload(self, positions, velocities, masses, ids, step: int):
         pos = np.ascontiguousarray(positions, dtype=np.float64)
@@ -187,6 +196,20 @@ class EngineContext:
         _lib.check(self._lib.mpcd_absorb(self.handle, C.c_void_p(int(recv_ptr) or None),
                                          int(n_recv), int(n_sent), _dev.stream()))
 
+    def step_rows(self, pos_in, vel_in, masses, pos_out, vel_out, step: int, want_drift: bool,
+                  want_com: bool = False):
+        """serial_collision_step rows: (n,3) inputs -> (n,3) outputs (host)."""
+        n = pos_in.shape[0]
+        drift = C.c_double(0.0)
+        m = None if self.uniform_mass else np.ascontiguousarray(masses, dtype=np.float64)
+        _lib.check(self._lib.mpcd_step_rows(
+            self.handle, pos_in.ctypes.data_as(_lib._d), vel_in.ctypes.data_as(_lib._d),
+            m.ctypes.data_as(_lib._d) if m is not None else None, n, int(step),
+            (_lib.STEP_WANT_DRIFT if want_drift else 0) | (_lib.STEP_WANT_COM if want_com else 0),
+            pos_out.ctypes.data_as(_lib._d), vel_out.ctypes.data_as(_lib._d), C.byref(drift),
+            _dev.stream()))
+        return drift.value
+
     def step_host(self, positions, velocities, masses, step: int, want_drift: bool,
                   want_com: bool = False):
         """serial_collision_step on host buffers (overwritten in place)."""
@@ -222,10 +245,15 @@ def _context_for(params: SimParams, n: int, mass_value):
 
 
 def _uniform_mass(masses: np.ndarray):
+    """The common mass when every particle has it, else None (a parallel
+    host scan: the pure function checks its input on every call)."""
     if masses.size == 0:
         return 1.0
-    m0 = masses[0]
-    return float(m0) if np.all(masses == m0) else None
+    m0 = float(masses[0])
+    if masses.size < (1 << 20):
+        return m0 if bool(np.all(masses == m0)) else None
+    t = _dev.torch()
+    return m0 if bool(t.from_numpy(masses).eq(m0).all()) else None
 
 
 def serial_collision_step(p: ParticleSet, params: SimParams, step: int, *,
@@ -233,20 +261,32 @@ def serial_collision_step(p: ParticleSet, params: SimParams, step: int, *,
     """One full step of the whole box on the GPU (engine.py:415-455).
 
     Same contract as the reference: returns (ParticleSet, drift | None,
-    (occupied_ids, com) | None) with rows in the input order.
+    (occupied_ids, com) | None) with rows in the input order; the input is
+    not modified.  The returned rows live in pooled page-locked host memory
+    (``_dev.pinned``): the kernels bin them straight from there on the next
+    call and write the next rows straight into another pooled block, so a
+    step loop moves each row over PCIe once per direction and copies nothing
+    on the host.  Pageable inputs are copied into a pooled block first.
     """
-    pos = np.array(p.positions, dtype=np.float64, order="C", copy=True)
-    vel = np.array(p.velocities, dtype=np.float64, order="C", copy=True)
     masses = np.ascontiguousarray(p.masses, dtype=np.float64)
-    ctx = _context_for(params, p.n, _uniform_mass(masses))
-    drift = ctx.step_host(pos, vel, masses, step, want_drift, want_com)
+    m0 = _uniform_mass(masses)
+    ctx = _context_for(params, p.n, m0)
+    pos_in = _dev.pinned_rows(p.positions)
+    vel_in = _dev.pinned_rows(p.velocities)
+    m_in = None if m0 is not None else _dev.pinned_rows(masses)
+    pos_out = _dev.pinned.empty((p.n, 3))
+    vel_out = _dev.pinned.empty((p.n, 3))
+    drift = ctx.step_rows(pos_in, vel_in, m_in, pos_out, vel_out, step, want_drift, want_com)
     com = ctx.read_com() if want_com else None
-    return ParticleSet(pos, vel, p.masses), (drift if want_drift else None), com
+    return ParticleSet(pos_out, vel_out, p.masses), (drift if want_drift else None), com
 
 
 # -------------------------------------------------------------- reports ---
 @dataclass(frozen=True)
 class ConservationReport:
+    """Whole-system sums of the last step (reference engine.py:463-477):
+    the same fields, and the same MpcdError for a non-finite value."""
+
     total_momentum: np.ndarray
     kinetic_energy: float
     total_mass: float
@@ -254,9 +294,10 @@ class ConservationReport:
     n_particles: int
 
     def __post_init__(self):
-        values = [*np.asarray(self.total_momentum).ravel(), self.kinetic_energy,
-                  self.total_mass, self.max_cell_drift]
-        if not all(math.isfinite(float(v)) for v in values):
+        scalars = np.array([self.kinetic_energy, self.total_mass, self.max_cell_drift],
+                           dtype=np.float64)
+        vec = np.asarray(self.total_momentum, dtype=np.float64).reshape(-1)
+        if not (np.isfinite(vec).all() and np.isfinite(scalars).all()):
             raise MpcdError("conservation report contains non-finite values")
 
 
@@ -324,6 +365,30 @@ class CudaRunner:
         self.ctx.close()
 
 
+class DecompositionAliasWarning(UserWarning):
+    """A reference decomposition option that this engine runs as an alias."""
+
+
+def _warn_aliases(params: SimParams, policy: str):
+    """Scheme A (engine.py:280-391) and the lazy policy (engine.py:134-146)
+    exist in the reference to limit split cells and halo traffic.  This
+    engine owns whole cells of the shifted grid, so no
+    cell is ever split: every scheme and policy runs the same decomposition,
+    with trajectories bitwise equal to the whole box."""
+    if params.n_ranks == 1:
+        return
+    if policy == POLICY_LAZY:
+        warnings.warn("policy='lazy' is an alias here: cell ownership migrates exactly the "
+                      "particles that change owner each step, with no guard band (the "
+                      "reference's lazy policy, engine.py:134-146, widens the halo instead)",
+                      DecompositionAliasWarning, stacklevel=3)
+    if params.scheme == SCHEME_MIGRATION:
+        warnings.warn("scheme='migration' (scheme A) runs the same cell-ownership "
+                      "decomposition as 'halo': no cell is split, so there are no halo "
+                      "moments to exchange (engine.py:280-391)",
+                      DecompositionAliasWarning, stacklevel=3)
+
+
 class Simulation:
     """A configured run: initialization, stepping, and collection (engine.py:494-641)."""
 
@@ -350,6 +415,7 @@ class Simulation:
                                       velocity_variance=velocity_variance, init=init)
         elif backend in (BACKEND_NCCL, BACKEND_SEQUENTIAL, BACKEND_PROCESS):
             from .distributed import NcclRunner, SequentialRunner
+            _warn_aliases(params, policy)
             cls = NcclRunner if backend == BACKEND_NCCL else SequentialRunner
             self._runner = cls(params, policy=policy, capture_drift=capture_drift,
                                capture_com=capture_com, velocity_variance=velocity_variance,
@@ -387,15 +453,21 @@ class Simulation:
         return self
 
     def advance(self, n_steps: int) -> "Simulation":
-        """n steps without per-step host synchronisation (diagnostics of the last only)."""
+        """n steps without per-step host synchronisation.
+
+        The first n - 1 steps run back to back on the device (their
+        diagnostics are not read); the last is an ordinary ``step()``, so
+        ``diagnostics``, ``drift_history``, ``com_captures``,
+        ``current_shift`` and ``conservation_report()`` describe it."""
         if n_steps <= 0:
             return self
         runner = self._runner
         if not isinstance(runner, CudaRunner):
             return self.run(n_steps)
-        flags = _lib.STEP_WANT_DRIFT if self.capture_drift else 0
-        runner.ctx.run(self.step_index, n_steps, flags)
-        self.step_index += n_steps
+        if n_steps > 1:
+            runner.ctx.run(self.step_index, n_steps - 1, 0)
+            self.step_index += n_steps - 1
+        self.step()
         return self
 
     def collect(self):

@@ -19,6 +19,13 @@ config1_L16.npz   BASELINE config 1 (16^3, 10/cell, 130 deg, seed 42):
                 initial state + per-step SHA-256 of the reference state,
                 cells, counts, permutation for 100 steps, diagnostics
 config2_L64.npz   64^3 seed 0: hash of the initial state and of 3 steps
+init_device.npz   init_system (particles.py:101-127) at 64^3 seed 0 and
+                16^3 x 12.5 seed 3: SHA-256 of the positions, every 1009th
+                velocity row, the subtracted mean (mean_init_velocity) --
+                pins the device init (positions bit-exact, velocities to
+                libm-vs-numpy ulps)
+bench_report.csv  the reference's emit_report of fixed records (+ .summary.txt)
+                and rank_dims_for(1..64) (bench_rank_dims.npy)
 decomposition.npz rank grids (neighbour tables, borders, coordinates),
                 base-3 side codes of random and border positions
 parallel_L8.npz   the reference's own rank-parallel step (backend
@@ -248,6 +255,50 @@ def make_config2(steps=3):
     np.savez_compressed(os.path.join(HERE, "config2_L64.npz"), **out)
 
 
+def make_init_device():
+    out = {}
+    for tag, params in (("L64", SimParams(edge_length=64, seed=0)),
+                        ("L16", SimParams(edge_length=16, seed=3, mean_density=12.5))):
+        p = particles.init_system(params)
+        out[f"{tag}_L"] = np.int64(params.edge_length)
+        out[f"{tag}_seed"] = np.int64(params.seed)
+        out[f"{tag}_density"] = np.float64(params.mean_density)
+        out[f"{tag}_n"] = np.int64(p.n)
+        out[f"{tag}_pos_sha"] = np.array(sha(p.positions))
+        out[f"{tag}_vel_rows"] = p.velocities[::1009].copy()
+        out[f"{tag}_pos_rows"] = p.positions[::1009].copy()
+        out[f"{tag}_mean"] = particles.mean_init_velocity(params)
+    # an explicit key: the reference still subtracts the (seed, step 0) mean
+    params = SimParams(edge_length=6, seed=5)
+    for step in (0, 3):
+        p = particles.init_system(params, key=rng.RngKey(seed=5, step=step))
+        out[f"key_step{step}_sha"] = np.array(sha(p.positions, p.velocities))
+    np.savez_compressed(os.path.join(HERE, "init_device.npz"), **out)
+
+
+def make_bench_report():
+    from mpcdsim import bench
+    recs = [bench.BenchRecord(L=16, ranks=1, scheme="halo", steps=3, seconds=0.1 + 1e-17,
+                              particles=40960, bytes_per_step=0.0, msgs_per_step=0.0,
+                              max_drift=1.3e-17),
+            bench.BenchRecord(L=16, ranks=2, scheme="halo", steps=3, seconds=0.07,
+                              particles=40960, bytes_per_step=2.0 ** 20 / 3,
+                              msgs_per_step=2.0, max_drift=2.2e-16),
+            bench.BenchRecord(L=16, ranks=3, scheme="migration", steps=3, seconds=0.0,
+                              particles=0, bytes_per_step=0.0, msgs_per_step=0.0,
+                              max_drift=0.0, error="ConfigError: rank_dims entry 3 does not "
+                              "divide 16, \"quoted\""),
+            bench.BenchRecord(L=32, ranks=1, scheme="halo", steps=20, seconds=1.2345678901234,
+                              particles=327680, bytes_per_step=0.0, msgs_per_step=0.0,
+                              max_drift=3.5e-15),
+            bench.BenchRecord(L=32, ranks=8, scheme="halo", steps=20, seconds=0.2,
+                              particles=327680, bytes_per_step=123456.5, msgs_per_step=7.5,
+                              max_drift=1e-300)]
+    bench.emit_report(recs, os.path.join(HERE, "bench_report.csv"))
+    np.save(os.path.join(HERE, "bench_rank_dims.npy"),
+            np.array([bench.rank_dims_for(n) for n in range(1, 65)], dtype=np.int64))
+
+
 def make_parallel(steps=5):
     """The reference's multi-rank path (engine.py:190-391 through
     runners.SequentialRunner) and its serial run, for the decomposed-box
@@ -312,6 +363,8 @@ if __name__ == "__main__":
     make_serial_small()
     make_config1()
     make_config2()
+    make_init_device()
+    make_bench_report()
     make_parallel()
     make_decomposition()
     with open(os.path.join(HERE, "PROVENANCE.txt"), "w") as f:

@@ -389,3 +389,103 @@ def test_full_size_step_bitexact_vs_oracle():
                            params.seed, 0)
     assert np.array_equal(p1.positions, r.positions)
     assert np.array_equal(p1.velocities, r.velocities)
+
+
+def _ulp(x):
+    x = np.abs(np.asarray(x, dtype=np.float64))
+    return np.spacing(np.maximum(x, np.finfo(np.float64).tiny))
+
+
+@pytest.mark.parametrize("tag", ["L16", "L64"])
+def test_device_init_matches_reference_init_system(tag):
+    """mpcd_init_device vs the reference's init_system (particles.py:101-127):
+    positions bit-exact (53-bit counter hash x box); velocities within 2 ulp
+    of max(|v|, 1).  A Box-Muller draw r cos(2 pi u) is a product of O(1)
+    factors from log/sqrt/cos, whose device and numpy results differ by an
+    ulp of those factors -- so the absolute error is ~ulp(1) even where the
+    product is small -- and the subtracted mean (a fixed-order device sum vs
+    numpy's chunked pairwise sum) differs by a few ulp of itself (~1e-18)."""
+    from conftest import golden
+    g = golden("init_device.npz")
+    L, seed, n = int(g[f"{tag}_L"]), int(g[f"{tag}_seed"]), int(g[f"{tag}_n"])
+    params = mp.SimParams(edge_length=L, seed=seed, mean_density=float(g[f"{tag}_density"]))
+    assert params.n_particles == n
+    ctx = engine.EngineContext(params.dims, 1.0, params.dt, params.alpha, params.seed,
+                               "splitmix", n, mass_value=1.0)
+    try:
+        ctx.init_device(n, 1.0, 0)
+        ids, p = ctx.download(id_order=True)
+    finally:
+        ctx.close()
+    assert np.array_equal(ids, np.arange(n))
+    assert sha(p.positions) == str(g[f"{tag}_pos_sha"])
+    assert np.array_equal(p.positions[::1009], g[f"{tag}_pos_rows"])
+    ref = g[f"{tag}_vel_rows"]
+    dev = np.abs(p.velocities[::1009] - ref)
+    tol = 2.0 * _ulp(np.maximum(np.abs(ref), 1.0))
+    stats = (f"max |dv| {dev.max():.3e}, identical {np.mean(dev == 0.0):.3f}, "
+             f"max |dv|/ulp(v) {(dev / _ulp(ref)).max():.1f}")
+    assert np.all(dev <= tol), stats
+    assert np.mean(dev == 0.0) > 0.5, stats
+    # the host init is numpy itself: bitwise
+    assert sha(mp.init_system(params).positions) == str(g[f"{tag}_pos_sha"])
+
+
+def test_config1_pcg32_100_steps_vs_oracle(g_config1):
+    """BASELINE config 1 literally: 16^3 x 10, 130 deg, prng="pcg32", seed 42,
+    100 steps through the resident engine; binning (cells, counts,
+    permutation) and state equal the oracle's at every step."""
+    params = mp.SimParams(edge_length=16, seed=42, prng="pcg32")
+    pos, vel = g_config1["pos0"], g_config1["vel0"]
+    n = pos.shape[0]
+    cs, sn = float(np.cos(params.alpha)), float(np.sin(params.alpha))
+    sim = _sim_from_state(params, pos, vel, capture_drift=True)
+    ctx = sim.runner.ctx
+    try:
+        for k in range(100):
+            cells, counts, offsets, perm = ctx.read_binning()
+            r = oracle.serial_step(pos, vel, np.ones(n), 16, 1.0, params.dt, cs, sn, params.seed,
+                                   k, prng="pcg32", want_drift=True, want_detail=True)
+            assert np.array_equal(cells, r.cells), k
+            assert np.array_equal(counts, r.counts), k
+            assert np.array_equal(perm, r.perm), k
+            d = sim.step()
+            ids, p = sim.collect()
+            pos, vel = r.positions, r.velocities
+            assert np.array_equal(p.positions, pos), k
+            assert np.array_equal(p.velocities, vel), k
+            assert d["max_cell_drift"] == pytest.approx(r.drift, rel=1e-6, abs=1e-15)
+    finally:
+        sim.close()
+
+
+def test_public_pure_step_zero_copy_chain():
+    """serial_collision_step returns its rows in pooled page-locked blocks and
+    reads such rows in place next call; the input is never modified, and a
+    chain of calls equals the oracle bit for bit (engine.py:415-455)."""
+    from paper_2212_11878_b200 import _dev
+
+    params = mp.SimParams(edge_length=12, seed=21)
+    p0 = mp.init_system(params)
+    keep = p0.copy()
+    assert not _dev.is_pinned(p0.positions)
+    q = p0
+    ref_pos, ref_vel = p0.positions, p0.velocities
+    cs, sn = float(np.cos(params.alpha)), float(np.sin(params.alpha))
+    for k in range(4):
+        q, _, _ = mp.serial_collision_step(q, params, k)
+        assert _dev.is_pinned(q.positions) and _dev.is_pinned(q.velocities)
+        r = oracle.serial_step(ref_pos, ref_vel, np.ones(p0.n), 12, 1.0, params.dt, cs, sn,
+                               params.seed, k)
+        ref_pos, ref_vel = r.positions, r.velocities
+        assert np.array_equal(q.positions, ref_pos) and np.array_equal(q.velocities, ref_vel), k
+    assert np.array_equal(p0.positions, keep.positions)
+    assert np.array_equal(p0.velocities, keep.velocities)
+    # random masses: the staged (non-uniform) path through the same call
+    m = np.random.default_rng(2).uniform(0.5, 2.0, size=p0.n)
+    pm = mp.ParticleSet(p0.positions, p0.velocities, m)
+    out, _, _ = mp.serial_collision_step(pm, params, 0)
+    r = oracle.serial_step(p0.positions, p0.velocities, m, 12, 1.0, params.dt, cs, sn,
+                           params.seed, 0)
+    assert np.array_equal(out.positions, r.positions)
+    assert np.array_equal(out.velocities, r.velocities)

@@ -154,3 +154,35 @@ def test_bench_reference_arm_runs_on_cpu():
     assert line["metric"] == "MPCD particle-steps/sec" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_init_system_explicit_key_matches_reference():
+    """init_system(params, key) subtracts the (params.seed, step 0) mean, as
+    the reference does (particles.py:101-127), for any key step."""
+    import hashlib
+
+    from conftest import golden
+    g = golden("init_device.npz")
+    params = mp.SimParams(edge_length=6, seed=5)
+    for step in (0, 3):
+        p = mp.init_system(params, key=mp.RngKey(seed=5, step=step))
+        h = hashlib.sha256()
+        for a in (p.positions, p.velocities):
+            h.update(np.ascontiguousarray(a).tobytes())
+        assert h.hexdigest() == str(g[f"key_step{step}_sha"]), step
+
+
+def test_lazy_policy_and_scheme_a_warn_as_aliases():
+    """policy='lazy' and scheme='migration' run the cell-ownership
+    decomposition: documented aliases that warn, never silently accepted."""
+    import warnings
+
+    from paper_2212_11878_b200 import engine
+    dec = mp.SimParams(edge_length=8, rank_dims=(2, 1, 1), scheme="migration")
+    with pytest.warns(mp.DecompositionAliasWarning) as rec:
+        engine._warn_aliases(dec, "lazy")
+    assert len(rec) == 2
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        engine._warn_aliases(mp.SimParams(edge_length=8, rank_dims=(2, 1, 1)), "immediate")
+        engine._warn_aliases(mp.SimParams(edge_length=8, scheme="migration"), "lazy")
