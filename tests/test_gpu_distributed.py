@@ -331,3 +331,63 @@ def test_full_size_two_domains_fused_equal_whole_box():
     assert np.array_equal(pa.positions, pb.positions)
     assert np.array_equal(pa.velocities, pb.velocities)
     assert all(d["crossings"] > 100_000 for d in diags)
+
+
+# -------------------------------- two NCCL ranks on two distinct GPUs ---
+def _nccl_worker(rank, world, port, out_dir, L, steps, migration):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(rank)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        params = mp.SimParams(edge_length=L, seed=13, rank_dims=(world, 1, 1))
+        with mp.Simulation(params, backend="nccl", init="device", capture_com=True,
+                           migration=migration) as sim:
+            diags = [sim.step() for _ in range(steps)]
+            # this rank's own particles only (no all-gather of the whole box)
+            (_, ids, p), = sim.runner._local_sets()
+            used = sim.runner.migration
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), ids=ids, pos=p.positions,
+                 vel=p.velocities, crossings=[d["crossings"] for d in diags], used=used)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available()
+                    or __import__("torch").cuda.device_count() < 2,
+                    reason="needs two GPUs (NCCL ranks on distinct devices)")
+@pytest.mark.parametrize("L,steps", [(64, 5), (256, 3)])
+@pytest.mark.parametrize("migration", ["fused", "exchange"])
+def test_two_gpus_nccl_equal_whole_box(tmp_path, L, steps, migration):
+    """Two NCCL ranks on two distinct GPUs (slab (2,1,1)): the fused migration
+    writes over NVLink peer memory with system-scope slot claims and an NCCL
+    all-reduce step fence; the exchange moves send buffers with NCCL
+    point-to-point.  Either way the collected state equals the whole box on
+    one GPU bit for bit (reference contract: engine.py:190-272,
+    test_engine.py:119-135, bound 1e-10 there; bitwise here)."""
+    import torch
+    import torch.multiprocessing as tmp_mp
+
+    tmp_mp.spawn(_nccl_worker, args=(2, _free_port(), str(tmp_path), L, steps, migration),
+                 nprocs=2, join=True)
+    torch.cuda.set_device(0)
+    with mp.Simulation(mp.SimParams(edge_length=L, seed=13), backend="cuda",
+                       init="device") as whole:
+        for _ in range(steps):
+            whole.step()
+        ids, p = whole.collect()
+    torch.cuda.empty_cache()
+    parts = [np.load(tmp_path / f"r{r}.npz") for r in range(2)]
+    got_ids = np.concatenate([o["ids"] for o in parts])
+    order = np.argsort(got_ids, kind="stable")
+    assert np.array_equal(got_ids[order], ids)
+    pos = np.concatenate([o["pos"].reshape(-1, 3) for o in parts])[order]
+    vel = np.concatenate([o["vel"].reshape(-1, 3) for o in parts])[order]
+    assert np.array_equal(pos, p.positions)
+    assert np.array_equal(vel, p.velocities)
+    for o in parts:
+        assert str(o["used"]) == migration
+        assert np.all(o["crossings"] > 0)

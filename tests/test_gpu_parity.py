@@ -399,12 +399,14 @@ def _ulp(x):
 @pytest.mark.parametrize("tag", ["L16", "L64"])
 def test_device_init_matches_reference_init_system(tag):
     """mpcd_init_device vs the reference's init_system (particles.py:101-127):
-    positions bit-exact (53-bit counter hash x box); velocities within 2 ulp
-    of max(|v|, 1).  A Box-Muller draw r cos(2 pi u) is a product of O(1)
-    factors from log/sqrt/cos, whose device and numpy results differ by an
-    ulp of those factors -- so the absolute error is ~ulp(1) even where the
-    product is small -- and the subtracted mean (a fixed-order device sum vs
-    numpy's chunked pairwise sum) differs by a few ulp of itself (~1e-18)."""
+    positions bit-exact (53-bit counter hash x box); velocities within 4 ulp
+    of the particle's Box-Muller radius r = sqrt(-2 log(1 - u1)) (floored at 1).
+    A draw r cos(2 pi u2) is the product of r (log, sqrt) and a cosine, whose
+    device (CUDA libdevice) and numpy results may each differ by an ulp; the
+    product's error is therefore ~ulp(r) |cos| + r ulp(cos) <= 2 ulp(r) plus
+    its own rounding, however small |v| is.  The subtracted mean (a
+    fixed-order device sum vs numpy's chunked pairwise sum) differs by a few
+    ulp of itself (~1e-18).  r is recomputed here from the same counters."""
     from conftest import golden
     g = golden("init_device.npz")
     L, seed, n = int(g[f"{tag}_L"]), int(g[f"{tag}_seed"]), int(g[f"{tag}_n"])
@@ -422,7 +424,14 @@ def test_device_init_matches_reference_init_system(tag):
     assert np.array_equal(p.positions[::1009], g[f"{tag}_pos_rows"])
     ref = g[f"{tag}_vel_rows"]
     dev = np.abs(p.velocities[::1009] - ref)
-    tol = 2.0 * _ulp(np.maximum(np.abs(ref), 1.0))
+    from paper_2212_11878_b200 import rng as R
+    state = R.key_state(seed, 0, R.Purpose.INIT, 0)
+    rows = np.arange(n)[::1009].astype(np.uint64)
+    cols = np.uint64(3 * n) + (np.uint64(3) * rows[:, None] + np.arange(3, dtype=np.uint64))
+    u1 = R.uniform_at(state, cols * np.uint64(2))
+    radius = np.sqrt(-2.0 * np.log(1.0 - u1))
+    assert np.all(np.abs(ref) <= radius + 1e-2)  # these draws, minus the O(n^-1/2) mean
+    tol = 4.0 * _ulp(np.maximum(radius, 1.0))
     stats = (f"max |dv| {dev.max():.3e}, identical {np.mean(dev == 0.0):.3f}, "
              f"max |dv|/ulp(v) {(dev / _ulp(ref)).max():.1f}")
     assert np.all(dev <= tol), stats
