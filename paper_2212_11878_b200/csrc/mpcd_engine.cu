@@ -350,6 +350,9 @@ using namespace mpcd;
 struct mpcd_ctx {
   mpcd_config cfg;
   int64_t C = 0, ntiles = 0, n = 0;
+  // every id of the (global) system is below this: set by upload / device
+  // init, which take the whole box's particles on every domain
+  int64_t id_bound = 0;
   uint32_t cap = 0, ovf_cap = 0, scratch_cap = 0;
   int tc = kTC;            // cells per tile of k_step (chosen from the density)
   uint32_t np_smem = 0;    // dense-tile particles staged in shared memory
@@ -362,7 +365,8 @@ struct mpcd_ctx {
   Recs ovf[2];
   uint32_t* ovf_cell[2] = {nullptr, nullptr};
   // [0..3] flags, [4,5] ovf_n, [6] scratch_n, [7] placed, [8] overflow
-  // bucket allocator, [9] dense staging exhausted
+  // bucket allocator, [9] dense staging exhausted, [10] a cell above the
+  // dense kernel's ranking limit
   uint32_t* small = nullptr;
   uint32_t* dense = nullptr;
   uint32_t* dense_bits = nullptr;
@@ -510,7 +514,7 @@ T* mapped(T* p) {
 // of an n-row array when it downloads in id order, so its ids must be a
 // permutation of 0..n-1 (a decomposed domain holds a subset of the global
 // ids and sorts them on the host instead).
-int validate_ids(const int64_t* ids, int64_t n, bool permutation) {
+int validate_ids(const int64_t* ids, int64_t n, bool permutation, int64_t* bound) {
   std::vector<int64_t> copy;
   const int64_t* h = ids;
   cudaPointerAttributes a;
@@ -522,8 +526,10 @@ int validate_ids(const int64_t* ids, int64_t n, bool permutation) {
     h = copy.data();
   }
   std::vector<uint8_t> seen(permutation ? n : 0, 0);
+  int64_t top = -1;
   for (int64_t i = 0; i < n; ++i) {
     const int64_t id = h[i];
+    top = std::max(top, id);
     if (id < 0 || id >= (1LL << 32))
       return fail(MPCD_ERR_CONFIG, "particle id %lld (row %lld) outside [0, 2^32)", (long long)id,
                   (long long)i);
@@ -534,6 +540,7 @@ int validate_ids(const int64_t* ids, int64_t n, bool permutation) {
       seen[id] = 1;
     }
   }
+  *bound = top + 1;
   return MPCD_OK;
 }
 
@@ -624,14 +631,18 @@ int check_flags(mpcd_ctx* c, cudaStream_t st) {
   uint32_t fl[kSmallWords];
   MPCD_CUDA(cudaMemcpyAsync(fl, flags_of(c), sizeof(fl), cudaMemcpyDeviceToHost, st));
   MPCD_CUDA(cudaStreamSynchronize(st));
-  if (fl[1] || fl[2] || fl[3] || fl[9]) {
+  if (fl[1] || fl[2] || fl[3] || fl[9] || fl[10]) {
     cudaMemsetAsync(flags_of(c) + 1, 0, 3 * sizeof(uint32_t), st);
-    cudaMemsetAsync(flags_of(c) + 9, 0, sizeof(uint32_t), st);
+    cudaMemsetAsync(flags_of(c) + 9, 0, 2 * sizeof(uint32_t), st);
     if (fl[1]) return fail(MPCD_ERR_RNG, "axis rejection sampling failed to terminate");
     if (fl[3])
       return fail(MPCD_ERR_TOPOLOGY, "a particle given to domain %d lies outside its cells",
                   (int)c->dom.rank);
     c->poisoned = true;  // particles were dropped: the state is no longer the system
+    if (fl[10])
+      return fail(MPCD_ERR_CAPACITY, "a cell holds more than %u particles (the dense-tile "
+                                     "kernel's ranking limit); particles were lost",
+                  (unsigned)kDenseMaxCell);
     if (fl[9])
       return fail(MPCD_ERR_CAPACITY, "a cluster of full tiles exceeds the dense-tile staging "
                                      "capacity (%u particles); particles were lost",
@@ -673,6 +684,10 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.scratch_src = c->scratch_src;
   A.scratch_cap = c->scratch_cap;
   A.np_smem = c->np_smem;
+  // ranks by the sign of a 32-bit difference need every id below 2^31 - 1:
+  // a whole-box context's ids are a permutation of 0..n-1, n <= capacity;
+  // a domain's are the global system's (bound set by upload / device init)
+  A.ids31 = (c->multi ? c->id_bound : g.capacity) <= (int64_t)kIds31Bound ? 1 : 0;
   A.tc = c->tc;
   A.cw = c->tc / kNCW;
   A.L0 = (int)g.dims[0]; A.L1 = (int)g.dims[1]; A.L2 = (int)g.dims[2];
@@ -1024,10 +1039,12 @@ int mpcd_upload(mpcd_ctx* c, const double* pos, const double* vel, const double*
   if (n > 0 && !c->cfg.uniform_mass && !mass) return fail(MPCD_ERR_CONFIG, "masses required");
   DeviceGuard dg(c->dev);
   cudaStream_t st = as_stream(stream);
+  int64_t bound = n;
   if (ids && n > 0) {
-    int rc = validate_ids(ids, n, !c->multi);
+    int rc = validate_ids(ids, n, !c->multi, &bound);
     if (rc) return rc;
   }
+  c->id_bound = bound;
   // retire whatever is resident
   for (int b = 0; b < 2; ++b) {
     MPCD_CUDA(cudaMemsetAsync(c->count[b], 0, sizeof(uint32_t) * c->C, st));
@@ -1285,6 +1302,7 @@ int mpcd_init_device(mpcd_ctx* c, int64_t n, double velocity_variance, int64_t s
     MPCD_CUDA(cudaMemsetAsync(ovf_n_of(c, b), 0, 4, st));
   }
   MPCD_CUDA(cudaMemsetAsync(placed_of(c), 0, 4, st));
+  c->id_bound = n;
   const int b = 0;
   if (n > 0) {
     double* part = nullptr;

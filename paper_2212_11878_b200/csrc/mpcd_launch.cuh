@@ -82,6 +82,11 @@ int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_
 
 template <int MODE>
 int64_t launch_mode_t(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
+#ifdef MPCD_ONLY_MAIN
+  // tuning builds (tools/build_variants.py): the binned unit-mass variant alone
+  if constexpr (MODE == kBinned) return launch_variant<true, true, false, false, kBinned>(A, nt, which, st);
+  else return -1;
+#else
 #define MPCD_V(U, M, D, C) \
   if (v.unit == U && v.umass == M && v.drift == D && v.com == C) \
     return launch_variant<U, M, D, C, MODE>(A, nt, which, st);
@@ -95,6 +100,7 @@ int64_t launch_mode_t(const StepArgs& A, int64_t nt, Variant v, int which, cudaS
   MPCD_V(false, false, true, false)
 #undef MPCD_V
   return launch_variant<false, false, true, true, MODE>(A, nt, which, st);
+#endif
 }
 #endif  // MPCD_STEP_VARIANTS_ONLY
 

@@ -81,6 +81,31 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_CNT_EVICT_LAST
 #define MPCD_CNT_EVICT_LAST 1
 #endif
+// producer: slot -> cell table written four slots per store
+#ifndef MPCD_CELLW
+#define MPCD_CELLW 1
+#endif
+// producer: two lanes per cell draw Marsaglia trials (tiles of <= 16 cells)
+#ifndef MPCD_AXPAIR
+#define MPCD_AXPAIR 1
+#endif
+// consumers: XOR-swizzled 16-byte halves of the 32-byte rows (bank conflicts)
+// (measured slower on B200: the kernel's time follows its instruction count,
+// and the swizzles' selects / column index math cost more issue slots than
+// the bank conflicts they remove -- profiles/r02_k_step.md)
+#ifndef MPCD_SWZ_W
+#define MPCD_SWZ_W 0
+#endif
+#ifndef MPCD_SWZ_T
+#define MPCD_SWZ_T 0
+#endif
+// consumers (one-domain mode): the last pass of a tile parks its collided
+// records in their own tile slots and stores them one tile later, so the
+// slot claims' round trip overlaps the next tile's rank/moment phases; the
+// tile buffer is released after that flush
+#ifndef MPCD_DEFER
+#define MPCD_DEFER 0
+#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -164,7 +189,8 @@ struct StepArgs {
   double* com_cap;            // COM: per cell com[3], count
   unsigned long long* drift_bits;
   // [0] dense tiles, [1] rng failure, [2] overflow list full, [3] routing
-  // error, [8] overflow bucket allocator, [9] dense staging exhausted
+  // error, [8] overflow bucket allocator, [9] dense staging exhausted,
+  // [10] a cell above kDenseMaxCell
   uint32_t* flags;
   uint32_t* dense;            // dense tile list (arrival order)
   uint32_t* dense_bits;       // one bit per tile: queued for k_step_dense
@@ -176,6 +202,7 @@ struct StepArgs {
   uint32_t* scratch_src;      // dense-kernel: source slot of each staged row
   uint32_t scratch_cap;
   uint32_t np_smem;           // particles of a dense tile staged in shared memory
+  int ids31;                  // every id < kIds31Bound: sign-bit ranking
   int tc, cw;                 // cells per tile, cells per consumer warp (tc / 4)
   int L0, L1, L2;
   int64_t C;
@@ -228,6 +255,11 @@ __device__ __forceinline__ uint64_t global_cell_id(const StepArgs& A, int64_t c)
 constexpr int kTC = MPCD_TC;    // most cells per tile (one producer lane per cell, <= 32)
 constexpr int kNT = 256;        // threads of the dense-tile CTA
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+// Ids below 2^31 - 1 rank by the sign bit of a 32-bit difference (one add +
+// one shift-add per compare instead of a compare + select + add); the
+// padding then carries kSentinel31, which never counts as smaller.
+constexpr uint32_t kIds31Bound = 0x7FFFFFFFu;
+constexpr uint32_t kSentinel31 = 0x7FFFFFFFu;
 constexpr int kPadBit = 0x80;  // slot-table flag of a padding slot
 constexpr int kDiagCols = 7;  // partial columns: px py pz sum(m v^2) mass collided migrated
 
@@ -247,8 +279,39 @@ __device__ __forceinline__ int cell_coord32(double x, double off, double a, int 
   return cell_coord_slow(t, L);
 }
 
+// floor(t) mod L for t = (x - off) / a with x in [0, box) (a wrapped
+// position) and |off| <= a/2: floor(t) is in [-1, L], mapped without a
+// branch.  Anything else (NaN / inf from a corrupt state) leaves the result
+// >= L, which cell_coord_fix sends through the exact general path.
+template <bool UNIT>
+__device__ __forceinline__ unsigned cell_coord_u(double x, double off, double a, int L, double& t) {
+  t = x - off;
+  if (!UNIT) t = t / a;  // IEEE division, as collision.py:132
+  const int c = __double2int_rd(t);
+  const unsigned u = (unsigned)(c < 0 ? c + L : c);  // -1 -> L - 1
+  return u == (unsigned)L ? 0u : u;                  // L -> 0
+}
+__device__ __forceinline__ unsigned cell_coord_fix(unsigned u, double t, int L) {
+  return u < (unsigned)L ? u : (unsigned)cell_coord_slow(t, L);
+}
+
+#ifndef MPCD_ONEBRANCH
+#define MPCD_ONEBRANCH 1
+#endif
 template <bool UNIT>
 __device__ __forceinline__ uint32_t next_cell(const StepArgs& A, double x, double y, double z) {
+  if (MPCD_ONEBRANCH) {  // one rarely taken branch for the three axes
+    double tx, ty, tz;
+    unsigned ix = cell_coord_u<UNIT>(x, A.off_next0, A.a, A.L0, tx);
+    unsigned iy = cell_coord_u<UNIT>(y, A.off_next1, A.a, A.L1, ty);
+    unsigned iz = cell_coord_u<UNIT>(z, A.off_next2, A.a, A.L2, tz);
+    if ((ix >= (unsigned)A.L0) | (iy >= (unsigned)A.L1) | (iz >= (unsigned)A.L2)) {
+      ix = cell_coord_fix(ix, tx, A.L0);
+      iy = cell_coord_fix(iy, ty, A.L1);
+      iz = cell_coord_fix(iz, tz, A.L2);
+    }
+    return (ix * (unsigned)A.L1 + iy) * (unsigned)A.L2 + iz;
+  }
   const unsigned ix = cell_coord32<UNIT>(x, A.off_next0, A.a, A.L0);
   const unsigned iy = cell_coord32<UNIT>(y, A.off_next1, A.a, A.L1);
   const unsigned iz = cell_coord32<UNIT>(z, A.off_next2, A.a, A.L2);
@@ -302,9 +365,25 @@ static __device__ __noinline__ void fused_put(const PeerBufs* peers, int b, uint
 template <bool UNIT>
 __device__ __forceinline__ bool next_cell_multi(const StepArgs& A, double x, double y, double z,
                                                 uint32_t& key, int& dest) {
-  const int gx = cell_coord32<UNIT>(x, A.off_next0, A.a, A.G0);
-  const int gy = cell_coord32<UNIT>(y, A.off_next1, A.a, A.G1);
-  const int gz = cell_coord32<UNIT>(z, A.off_next2, A.a, A.G2);
+  int gx, gy, gz;
+  if (MPCD_ONEBRANCH) {
+    double tx, ty, tz;
+    unsigned ux = cell_coord_u<UNIT>(x, A.off_next0, A.a, A.G0, tx);
+    unsigned uy = cell_coord_u<UNIT>(y, A.off_next1, A.a, A.G1, ty);
+    unsigned uz = cell_coord_u<UNIT>(z, A.off_next2, A.a, A.G2, tz);
+    if ((ux >= (unsigned)A.G0) | (uy >= (unsigned)A.G1) | (uz >= (unsigned)A.G2)) {
+      ux = cell_coord_fix(ux, tx, A.G0);
+      uy = cell_coord_fix(uy, ty, A.G1);
+      uz = cell_coord_fix(uz, tz, A.G2);
+    }
+    gx = (int)ux;
+    gy = (int)uy;
+    gz = (int)uz;
+  } else {
+    gx = cell_coord32<UNIT>(x, A.off_next0, A.a, A.G0);
+    gy = cell_coord32<UNIT>(y, A.off_next1, A.a, A.G1);
+    gz = cell_coord32<UNIT>(z, A.off_next2, A.a, A.G2);
+  }
   const unsigned lx = (unsigned)(gx - A.o0), ly = (unsigned)(gy - A.o1), lz = (unsigned)(gz - A.o2);
   if (lx < (unsigned)A.L0 && ly < (unsigned)A.L1 && lz < (unsigned)A.L2) {
     key = (lx * (unsigned)A.L1 + ly) * (unsigned)A.L2 + lz;
@@ -331,6 +410,22 @@ __device__ __forceinline__ double wrap_fast(double x, double box) {
   }
   if (x >= box && x < 2.0 * box) return x - box;
   return wrap_slow(x, box);
+}
+
+// Three coordinates with one rarely taken branch: x in [+0, box) is its own
+// remainder (the bit-pattern compare of wrap_fast); any other value takes
+// wrap_fast's full ladder.
+__device__ __forceinline__ void wrap3(double& x, double& y, double& z, double bx, double by,
+                                      double bz) {
+  typedef unsigned long long u64;
+  const bool fx = (u64)__double_as_longlong(x) < (u64)__double_as_longlong(bx);
+  const bool fy = (u64)__double_as_longlong(y) < (u64)__double_as_longlong(by);
+  const bool fz = (u64)__double_as_longlong(z) < (u64)__double_as_longlong(bz);
+  if (!(fx & fy & fz)) {
+    x = wrap_fast(x, bx);
+    y = wrap_fast(y, by);
+    z = wrap_fast(z, bz);
+  }
 }
 
 // numpy pairwise leaf, compile-time stride, 32-bit indices
@@ -408,6 +503,13 @@ __device__ __forceinline__ void claim_slot(const StepArgs& A, bool active, uint3
   grp = 0u;
   base = 0u;
   if (MPCD_NOAGG) {  // one atomic per particle: the slot itself
+#ifdef MPCD_ABL_NOATOM  // timing ablation only (wrong results): no claim round trip
+    if (active) {  // the counts stay right (no-return reduction), the slot is made up
+      atomicAdd(&A.count_out[key], 1u);
+      base = (key ^ threadIdx.x) & 7u;
+    }
+    return;
+#endif
     if (active) base = count_claim<SYS>(&A.count_out[key], 1u);
     return;
   }
@@ -431,6 +533,9 @@ __device__ __forceinline__ void finish_slot(const StepArgs& A, uint32_t key, uns
     slot = base + (uint32_t)__popc(grp & ((1u << lane) - 1u));
   }
   if (slot < A.cap) {
+#ifdef MPCD_ABL_NOSTORE  // timing ablation only (wrong results): no record stores
+    if (slot == 0xFFFFFFF0u)
+#endif
     store_rec(A.out, (uint64_t)key * A.cap + slot, o[0], o[1], o[2], id, o[3], o[4], o[5], m);
   } else {  // full cell: overflow list (gathered by the dense kernel next step)
     const uint32_t q = SYS ? atomicAdd_system(A.ovf_n_out, 1u) : atomicAdd(A.ovf_n_out, 1u);
@@ -516,6 +621,83 @@ __device__ __forceinline__ void sts_row32(void* base, int row, double2 lo, doubl
   double2* p = reinterpret_cast<double2*>(base) + 2 * row;
   p[0] = lo;
   p[1] = hi;
+}
+
+// 32-byte rows read by consecutive lanes: rows r and r + 4 share a bank
+// group, so eight lanes reading the same half of eight rows conflict 2-way.
+// Swizzled rows (the warp-private staging W.val) keep half h of row r at
+// 16 * (h ^ sw(r)) with sw(r) = (r >> 2) & 1, so the same access reaches all
+// eight bank groups; a column element (r, c) is double c ^ 2 sw(r) of row r.
+__device__ __forceinline__ int row_sw(int row) { return MPCD_SWZ_W ? (row >> 2) & 1 : 0; }
+__device__ __forceinline__ void lds_row32w(const double* base, int row, double2& lo, double2& hi) {
+  const double2* p = reinterpret_cast<const double2*>(base) + 2 * row;
+  const int h = row_sw(row);
+  lo = p[h];
+  hi = p[h ^ 1];
+}
+__device__ __forceinline__ void sts_row32w(double* base, int row, double2 lo, double2 hi) {
+  double2* p = reinterpret_cast<double2*>(base) + 2 * row;
+  const int h = row_sw(row);
+  p[h] = lo;
+  p[h ^ 1] = hi;
+}
+// Rows laid out by the copy engine (the tile buffer, unswizzled): lanes with
+// sw(r) = 1 load the high half first, which spreads the eight lanes of each
+// access over all bank groups; the halves are put back in place by selects.
+__device__ __forceinline__ void lds_row32t(const void* base, int row, double2& lo, double2& hi) {
+  const double2* p = reinterpret_cast<const double2*>(base) + 2 * row;
+  if (!MPCD_SWZ_T) {
+    lo = p[0];
+    hi = p[1];
+    return;
+  }
+  const bool h = (row >> 2) & 1;
+  const double2 a = p[h ? 1 : 0], b = p[h ? 0 : 1];
+  lo.x = h ? b.x : a.x;
+  lo.y = h ? b.y : a.y;
+  hi.x = h ? a.x : b.x;
+  hi.y = h ? a.y : b.y;
+}
+
+// numpy pairwise leaf over column c of swizzled rows row0 + 0 .. n - 1 (the
+// association of pw_leaf, n < 129)
+__device__ __forceinline__ double pw_leaf_w(const double* base, int row0, int c, int n) {
+  auto at = [&](int i) {
+    const int r = row0 + i;
+    return base[r * 4 + (c ^ (row_sw(r) << 1))];
+  };
+  if (n < 16) {
+    if (n < 8) {
+      double res = 0.0;
+#pragma unroll
+      for (int i = 0; i < 7; ++i)
+        if (i < n) res += at(i);
+      return res;
+    }
+    double res = ((at(0) + at(1)) + (at(2) + at(3))) + ((at(4) + at(5)) + (at(6) + at(7)));
+#pragma unroll
+    for (int i = 8; i < 15; ++i)
+      if (i < n) res += at(i);
+    return res;
+  }
+  double r0 = at(0), r1 = at(1), r2 = at(2), r3 = at(3);
+  double r4 = at(4), r5 = at(5), r6 = at(6), r7 = at(7);
+  int i = 8;
+  const int full = n - (n & 7);
+  for (; i < full; i += 8) {
+    r0 += at(i); r1 += at(i + 1); r2 += at(i + 2); r3 += at(i + 3);
+    r4 += at(i + 4); r5 += at(i + 5); r6 += at(i + 6); r7 += at(i + 7);
+  }
+  double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) res += at(i);
+  return res;
+}
+// np.add.reduceat of column c over the k swizzled rows from row0 (k <= kSlotsW)
+__device__ __forceinline__ double reduceat_wcol(const double* base, int row0, int c, int k) {
+  if (k <= 0) return 0.0;
+  const double first = base[row0 * 4 + (c ^ (row_sw(row0) << 1))];
+  if (k == 1) return first;
+  return first + pw_leaf_w(base, row0 + 1, c, k - 1);
 }
 
 // ------------------------------------------------------------ TMA helpers --
@@ -735,8 +917,61 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   }
 #endif
   // slot -> cell, bit 7 set on a padding slot
+#if MPCD_CELLW
+  // four slots per 32-bit store (a cell's padded run starts and ends on a
+  // multiple of 4 slots)
+  for (uint32_t j = excl; j < incl; j += 4) {
+    const uint32_t real = k - min(k, j - excl);  // real slots from j on
+    const uint32_t pad = real >= 4u ? 0u : (0x80808080u << (8u * real));
+    *reinterpret_cast<uint32_t*>(B.cell + j) = ((uint32_t)lane * 0x01010101u) | pad;
+  }
+#else
   for (uint32_t j = excl; j < incl; ++j) B.cell[j] = (uint8_t)(lane | (j - excl < k ? 0 : kPadBit));
+#endif
   // rotation axes (collision.py:217-250), keyed by the global cell id
+#ifdef MPCD_ABL_NOAXIS  // timing ablation only (wrong results): a fixed axis
+  if (lane < kTC) {
+    double* ax = B.ax + lane * 4;
+    ax[0] = 0.0; ax[1] = 0.6; ax[2] = 0.8;
+  }
+  if (0)
+#endif
+#if MPCD_AXPAIR
+  if (TILE_CELLS(A) <= 16 && A.prng == kSplitmix) {
+    // two lanes per cell draw Marsaglia trials 2i and 2i + 1 at once (the
+    // counter generator needs no sequential state); the first accepted
+    // trial in trial order wins, exactly as the one-lane loop
+    const int cell = lane >> 1, s = lane & 1;
+    const uint32_t ccnt = __shfl_sync(0xffffffffu, cnt, cell);
+    bool done = !(cell < TILE_CELLS(A) && ccnt > 0u);
+    const uint64_t key = done ? 0ull : key_from_prefix(A.axis_prefix, global_cell_id<MODE>(A, c0 + cell));
+    double* ax = B.ax + cell * 4;
+    if (s == 0 && cell < TILE_CELLS(A)) ax[0] = ax[1] = ax[2] = 0.0;
+    __syncwarp();  // the zeros precede a partner lane's axis
+    for (int i = 0; i < kMaxAxisTrials / 2; ++i) {
+      if (!__any_sync(0xffffffffu, !done)) break;
+      double x = 0.0, y = 0.0, rsq = 1.0;
+      if (!done) {
+        const uint64_t t = 2ull * (uint64_t)(2 * i + s);
+        x = 2.0 * uniform_at(key, t) - 1.0;
+        y = 2.0 * uniform_at(key, t + 1ull) - 1.0;
+        rsq = x * x + y * y;
+      }
+      const unsigned acc = __ballot_sync(0xffffffffu, !done && rsq < 1.0);
+      const unsigned pair = (acc >> (lane & ~1)) & 3u;
+      if (!done && pair) {
+        if (s == ((pair & 1u) ? 0 : 1)) {  // the earlier accepted trial of the pair
+          const double root = sqrt(1.0 - rsq);
+          ax[0] = (2.0 * x) * root;
+          ax[1] = (2.0 * y) * root;
+          ax[2] = 1.0 - 2.0 * rsq;
+        }
+        done = true;
+      }
+    }
+    if (!done && s == 0) atomicOr(&A.flags[1], 1u);  // 128 trials rejected
+  } else
+#endif
   if (lane < kTC) {
     double* ax = B.ax + lane * 4;
     ax[0] = ax[1] = ax[2] = 0.0;
@@ -747,11 +982,50 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane == 0) mbar_arrive(full);  // release: layout, table and axes written
 }
 
+// Stores a warp left pending (MPCD_DEFER): rows r with bit r of `mask` hold
+// a collided record parked in slot j0 + lane + 32 r of tile buffer `buf`,
+// bound for slot base[r] of next-step cell key[r].
+template <int R>
+struct Deferred {
+  uint32_t key[R], base[R];
+  unsigned mask;  // this lane's rows
+  int j0;
+  int buf;        // tile buffer still held (-1: none)
+};
+
+// Store the parked records, then hand the tile buffer back to the producer.
+template <int R, class Smem>
+__device__ __forceinline__ void flush_deferred(const StepArgs& A, Smem& S, Deferred<R>& D) {
+  if (D.buf < 0) return;
+  const int lane = threadIdx.x & 31;
+  TileBuf& P = S.buf[D.buf];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if ((D.mask >> r) & 1u) {
+      double2 p01, p23, v01, v23;
+      lds_row32(P.p, D.j0 + lane + 32 * r, p01, p23);
+      lds_row32(P.v, D.j0 + lane + 32 * r, v01, v23);
+      const double o[6] = {p01.x, p01.y, p23.x, v01.x, v01.y, v23.x};
+      finish_slot<false>(A, D.key[r], 0u, D.base[r], o, bits_id(p23.y), v23.y);
+    }
+  }
+  fence_proxy_async();  // the parked slots' generic writes precede the next TMA fill
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&S.empty[D.buf]);
+  D.buf = -1;
+  D.mask = 0u;
+}
+
 // One consumer warp's cells of one tile: every phase, R slot rows per lane.
+// `defer` (one-domain mode, last pass of the tile): park the collided
+// records instead of storing them, into D; a pending D of the previous tile
+// is flushed after this pass's moments.
 template <int R, bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE, class Smem>
 __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBuf& T,
                                               WarpScratch& W, int64_t c0, int cw0,
-                                              int ncw, int j0, int j1, double* acc) {
+                                              int ncw, int j0, int j1, double* acc,
+                                              uint32_t& ncoll, Deferred<R>& D, bool defer,
+                                              int tb) {
   constexpr bool BYID = MODE == kById;
   const int lane = threadIdx.x & 31;
 #ifdef MPCD_TIMING
@@ -762,16 +1036,20 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   // phase 1: ids in slot order (sentinel in the padding), warp-local rows
   int lq[R];  // cell of the row inside the warp (0..3)
   bool real[R];
+  uint32_t myid[R];  // the row's id (kept: phase 2 ranks it)
+  const uint32_t pad_id = A.ids31 ? kSentinel31 : kSentinel;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int jl = lane + 32 * r, j = j0 + jl;
     real[r] = false;
     lq[r] = 0;
+    myid[r] = pad_id;
     if (j < j1) {
       const int cj = T.cell[j];
       lq[r] = (cj & ~kPadBit) - cw0;
       real[r] = !(cj & kPadBit);
-      W.id[jl] = real[r] ? T.p[j].id : kSentinel;
+      if (real[r]) myid[r] = T.p[j].id;
+      W.id[jl] = myid[r];
     }
   }
   __syncwarp();
@@ -788,21 +1066,35 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       const int jl = lane + 32 * r;
       const int q = lq[r];
       const int lo = (int)T.off[cw0 + q] - j0, hi = (int)T.off[cw0 + q + 1] - j0;
-      const uint32_t me = W.id[jl];
+      const uint32_t me = myid[r];
       uint32_t rank = 0;
+#ifdef MPCD_ABL_NORANK  // timing ablation only (wrong results): slot order
+      rank = (uint32_t)(jl - lo);
+      if (0)
+#endif
+      if (A.ids31) {
 #pragma unroll 1
-      for (int s = lo; s < hi; s += 4) {
-        const uint4 w = *reinterpret_cast<const uint4*>(W.id + s);
-        rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
+        for (int s = lo; s < hi; s += 4) {
+          const uint4 w = *reinterpret_cast<const uint4*>(W.id + s);
+          // both below 2^31: w < me is the sign bit of w - me
+          rank += ((w.x - me) >> 31) + ((w.y - me) >> 31) + ((w.z - me) >> 31) +
+                  ((w.w - me) >> 31);
+        }
+      } else {
+#pragma unroll 1
+        for (int s = lo; s < hi; s += 4) {
+          const uint4 w = *reinterpret_cast<const uint4*>(W.id + s);
+          rank += (w.x < me) + (w.y < me) + (w.z < me) + (w.w < me);
+        }
       }
       row[r] = lo + (int)rank + q;
       double2 v01, v23;  // vx vy | vz m
-      lds_row32(T.v, j0 + jl, v01, v23);
+      lds_row32t(T.v, j0 + jl, v01, v23);
       const double m = UMASS ? A.m0 : v23.y;
       if (UMASS && A.m0 == 1.0)  // unit masses: m v == v exactly, no multiplies
-        sts_row32(W.val, row[r], v01, make_double2(v23.x, 1.0));
+        sts_row32w(W.val, row[r], v01, make_double2(v23.x, 1.0));
       else
-        sts_row32(W.val, row[r], make_double2(m * v01.x, m * v01.y), make_double2(m * v23.x, m));
+        sts_row32w(W.val, row[r], make_double2(m * v01.x, m * v01.y), make_double2(m * v23.x, m));
     }
   }
   __syncwarp();
@@ -817,7 +1109,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     double mom = 0.0;
     if (mine) {
       const int lc = cw0 + q;
-      mom = reduceat_col<4>(W.val + ((int)T.off[lc] - j0 + q) * 4 + comp, (int)T.cnt[lc]);
+      mom = reduceat_wcol(W.val, (int)T.off[lc] - j0 + q, comp, (int)T.cnt[lc]);
     }
     const double mass = __shfl_sync(0xffffffffu, mom, lane | 3);
     if (mine) {
@@ -827,12 +1119,13 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       if (comp < 3) W.com[q * 4 + comp] = c;
       else {
         acc[4] += mass;
-        acc[5] += (double)T.cnt[cw0 + q];  // particles collided
+        ncoll += T.cnt[cw0 + q];  // particles collided
       }
       if (COM) A.com_cap[(c0 + cw0 + q) * 4 + comp] = c;
     }
   }
   __syncwarp();
+  if (MPCD_DEFER && MODE == kBinned) flush_deferred<R>(A, S, D);
   MPCD_PROBE(3);
 
   // phase 4: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
@@ -861,17 +1154,24 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       const int j = j0 + lane + 32 * r;
 #endif
       double2 p01, p23, v01, v23;  // x y | z id, vx vy | vz m
-      lds_row32(T.p, j, p01, p23);
-      lds_row32(T.v, j, v01, v23);
+      lds_row32t(T.p, j, p01, p23);
+      lds_row32t(T.v, j, v01, v23);
       double2 c01, c2, a01, a2;
       lds_row32(W.com + lq[r] * 4, 0, c01, c2);
       lds_row32(T.ax + (cw0 + lq[r]) * 4, 0, a01, a2);
       const double cx[3] = {c01.x, c01.y, c2.x}, ax[3] = {a01.x, a01.y, a2.x};
       double v[3] = {v01.x, v01.y, v23.x}, w[3];
       rotate(v, cx, ax, A.cs, A.sn, w);
-      o[r][0] = wrap_fast(p01.x + w[0] * A.dt, A.box0);
-      o[r][1] = wrap_fast(p01.y + w[1] * A.dt, A.box1);
-      o[r][2] = wrap_fast(p23.x + w[2] * A.dt, A.box2);
+      if (MPCD_ONEBRANCH) {
+        o[r][0] = p01.x + w[0] * A.dt;
+        o[r][1] = p01.y + w[1] * A.dt;
+        o[r][2] = p23.x + w[2] * A.dt;
+        wrap3(o[r][0], o[r][1], o[r][2], A.box0, A.box1, A.box2);
+      } else {
+        o[r][0] = wrap_fast(p01.x + w[0] * A.dt, A.box0);
+        o[r][1] = wrap_fast(p01.y + w[1] * A.dt, A.box1);
+        o[r][2] = wrap_fast(p23.x + w[2] * A.dt, A.box2);
+      }
       o[r][3] = w[0]; o[r][4] = w[1]; o[r][5] = w[2];
       pid[r] = bits_id(p23.y);
       mm[r] = UMASS ? A.m0 : v23.y;
@@ -891,10 +1191,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
       if (real[r]) {
         if (UMASS && A.m0 == 1.0)
-          sts_row32(W.val, row[r], make_double2(w[0], w[1]), make_double2(w[2], ke));
+          sts_row32w(W.val, row[r], make_double2(w[0], w[1]), make_double2(w[2], ke));
         else
-          sts_row32(W.val, row[r], make_double2(m * w[0], m * w[1]),
-                    make_double2(m * w[2], m * ke));
+          sts_row32w(W.val, row[r], make_double2(m * w[0], m * w[1]),
+                     make_double2(m * w[2], m * ke));
       }
       if (decomposed(MODE) && real[r] && !stay[r]) {
         // a leaver: park its record in its own tile slot (dest in the pad
@@ -937,7 +1237,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     if (real[r]) {
       const int jl = lane + 32 * r;
       double2 a, c;
-      lds_row32(W.val, jl + lq[r], a, c);
+      lds_row32w(W.val, jl + lq[r], a, c);
       acc[0] += a.x; acc[1] += a.y; acc[2] += c.x; acc[3] += c.y;
     }
   }
@@ -951,7 +1251,25 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   }
   MPCD_PROBE(6);
 #endif
-  if (!BYID) {
+  if (MPCD_DEFER && MODE == kBinned && defer) {
+    // park: each row's record in its own slot (read by this lane only)
+    unsigned mask = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (stay[r]) {
+        const int j = j0 + lane + 32 * r;
+        sts_row32(T.p, j, make_double2(o[r][0], o[r][1]),
+                  make_double2(o[r][2], id_bits(pid[r])));
+        sts_row32(T.v, j, make_double2(o[r][3], o[r][4]), make_double2(o[r][5], mm[r]));
+        D.key[r] = key[r];
+        D.base[r] = base[r];
+        mask |= 1u << r;
+      }
+    }
+    D.mask = mask;
+    D.j0 = j0;
+    D.buf = tb;
+  } else if (!BYID) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (stay[r]) finish_slot<MODE == kFused>(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
@@ -985,7 +1303,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     double post = 0.0;
     if (lane < 4 * kCW && q < ncw) {
       const int lc = cw0 + q;
-      post = reduceat_col<4>(W.val + ((int)T.off[lc] - j0 + q) * 4 + comp, (int)T.cnt[lc]);
+      post = reduceat_wcol(W.val, (int)T.off[lc] - j0 + q, comp, (int)T.cnt[lc]);
     }
     double* P = S.post + cw0 * 4;  // this pass's cells only
     if (lane < 4 * ncw) P[lane] = post;
@@ -1025,12 +1343,19 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     const uint64_t pol = policy_evict_normal();
     int64_t tile = blockIdx.x;
     uint32_t cnt = tile_count<FIX>(A, tile, ntiles);
+    // buffer b of round `ph` (the parity of i / kStages), kept incrementally:
+    // no 64-bit division per tile
+    int b = 0;
+    uint32_t ph = 0u;
     for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
-      const int b = (int)(i % kStages);
       const uint32_t cnt_next = tile_count<FIX>(A, tile + G, ntiles);  // in flight meanwhile
-      if (i >= kStages) mbar_wait(&S.empty[b], (uint32_t)((i / kStages) - 1) & 1u);
+      if (i >= kStages) mbar_wait(&S.empty[b], ph ^ 1u);
       prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
       cnt = cnt_next;
+      if (++b == kStages) {
+        b = 0;
+        ph ^= 1u;
+      }
     }
     return;
   }
@@ -1040,21 +1365,32 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   const int cw0 = warp * WARP_CELLS(A);  // this warp's first cell of every tile
   // px py pz sum(m v^2) mass, particles collided, particles sent to other ranks
   double acc[kDiagCols] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  uint32_t ncoll = 0u;  // particles collided by this thread's cell lanes (acc[5])
+  Deferred<kRowsW> D;
+  D.buf = -1;
+  D.mask = 0u;
+  D.j0 = 0;
   int64_t tile = blockIdx.x;
-  for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
-    const int b = (int)(i % kStages);
+  int b = 0;
+  uint32_t ph = 0u;
+  for (int64_t i = 0; tile < ntiles; ++i, tile += G, b = (b + 1 == kStages) ? 0 : b + 1,
+               ph ^= (b == 0) ? 1u : 0u) {
     TileBuf& T = S.buf[b];
 #ifdef MPCD_TIMING
     const long long tw0 = clock64();
 #endif
-    mbar_wait(&S.full[b], (uint32_t)(i / kStages) & 1u);
+    mbar_wait(&S.full[b], ph);
 #ifdef MPCD_TIMING
     if (lane == 0) S.tim[warp][8] += (unsigned long long)(clock64() - tw0);
     if (lane == 0) S.tim[warp][9] += 1ull;
 #endif
     const int64_t c0 = tile * TILE_CELLS(A);
-    const int ncw = T.skip ? 0 : (int)max((int64_t)0, min((int64_t)WARP_CELLS(A), A.C - c0 - cw0));
+    int ncw = WARP_CELLS(A);
+    if (c0 + TILE_CELLS(A) > A.C)  // the box's last, partial tile
+      ncw = (int)max((int64_t)0, min((int64_t)ncw, A.C - c0 - cw0));
+    if (T.skip) ncw = 0;
     if (ncw == 0) {
+      if (MPCD_DEFER && MODE == kBinned) flush_deferred<kRowsW>(A, S, D);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[b]);
       continue;
@@ -1071,12 +1407,15 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
         while (g1 < gend && T.off[g1 + 1] - T.off[g0] <= (uint32_t)kSlotsW) ++g1;
       }
       consume_cells<kRowsW, UNIT, UMASS, DRIFT, COM, MODE>(A, S, T, W, c0, g0, g1 - g0,
-                                                           (int)T.off[g0], (int)T.off[g1], acc);
+                                                           (int)T.off[g0], (int)T.off[g1], acc,
+                                                           ncoll, D, g1 == gend, b);
       __syncwarp();  // W is rewritten by the next pass
       g0 = g1;
     }
-    if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
+    // the tile buffer is free for the producer (after the deferred stores)
+    if (!(MPCD_DEFER && MODE == kBinned) && lane == 0) mbar_arrive(&S.empty[b]);
   }
+  if (MPCD_DEFER && MODE == kBinned) flush_deferred<kRowsW>(A, S, D);
 #ifdef MPCD_TIMING
   if (lane < 10) atomicAdd(&g_phase_cycles[lane], S.tim[warp][lane]);
 #endif
@@ -1084,6 +1423,7 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   // system-wide before the step fence (the all-reduce that follows the step)
   if (A.peers) __threadfence_system();
   // CTA partials: fixed-order block reduction of the per-thread sums
+  acc[5] = (double)ncoll;
 #pragma unroll
   for (int q = 0; q < kDiagCols; ++q)
     for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
@@ -1156,6 +1496,12 @@ __global__ void __launch_bounds__(256) k_ovf_bucket(const StepArgs A) {
 
 #endif  // MPCD_STEP_VARIANTS_ONLY
 
+// Largest cell occupancy the dense-tile kernel ranks (k^2 / 256 compares per
+// CTA: ~16 M at the limit); a step that meets a bigger cell fails with
+// MPCD_ERR_CAPACITY.  65536 particles in one cell is 6500x the mean density
+// of the benchmark configurations.
+constexpr uint32_t kDenseMaxCell = 65536;
+
 // Bytes of dynamic shared memory k_step_dense stages `np` particles in.
 __host__ __device__ constexpr size_t dense_smem_bytes(uint32_t np) {
   return (size_t)np * (4 * sizeof(double) + 2 * sizeof(uint32_t));
@@ -1199,7 +1545,13 @@ __global__ void __launch_bounds__(kNT) k_step_dense(const StepArgs A) {
       s_off[kTC] = acc;
       s_mode = 0;
       s_base = 0;
-      if (acc > A.np_smem) {
+      uint32_t biggest = 0;
+      for (int lc = 0; lc < nc; ++lc) biggest = max(biggest, s_cnt[lc]);
+      if (biggest > kDenseMaxCell) {
+        // the in-cell ranking is O(k^2 / threads): refuse rather than stall
+        s_mode = -1;
+        atomicOr(&A.flags[10], 1u);
+      } else if (acc > A.np_smem) {
         const uint32_t b = atomicAdd(A.scratch_n, acc);
         if ((uint64_t)b + acc <= (uint64_t)A.scratch_cap) {
           s_mode = 1;

@@ -226,3 +226,25 @@ def test_upload_rejects_bad_ids():
         assert np.array_equal(p.positions[perm], pos)
     finally:
         ctx.close()
+
+
+def test_cell_beyond_dense_ranking_limit_fails_loudly():
+    """70,000 particles in one cell (above k_step_dense's 65,536 ranking
+    limit, mpcd_step.cuh kDenseMaxCell): MPCD_ERR_CAPACITY rather than an
+    O(k^2) stall; a sane state steps again after a fresh upload."""
+    n = 70_000
+    L = 16
+    ctx = engine.EngineContext((L, L, L), 1.0, 0.1, np.radians(130.0), 1, "splitmix", 4 * n,
+                               mass_value=1.0)
+    try:
+        vel = np.random.default_rng(0).normal(size=(n, 3))
+        with pytest.raises(mp.MpcdError, match="ranking limit"):
+            ctx.upload(np.full((n, 3), 3.5), vel, None, None, 0)
+            ctx.step(0)
+            ctx.read_diag()
+        ok = np.random.default_rng(1).uniform(0, L, size=(n, 3))
+        ctx.upload(ok, vel, None, None, 0)
+        ctx.step(0)
+        assert ctx.read_diag().n == n
+    finally:
+        ctx.close()

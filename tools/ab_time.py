@@ -59,9 +59,13 @@ def main():
     ap.add_argument("--density", type=float, default=10.0)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--hash", type=int, default=1, help="compare the final state across libs")
+    ap.add_argument("--split", type=int, default=1, help="per-kernel ms: k_step, dense, diag")
     a = ap.parse_args()
     torch.cuda.init()
     res = {p: [] for p in a.libs}
+    hashes = {}
+    splits = {}
     step0 = {p: 0 for p in a.libs}
     for r in range(a.rounds):
         for p in a.libs:
@@ -72,6 +76,16 @@ def main():
                 os.environ[k] = v
             lib, h, n, st = make(path, a.L, a.density)
             assert lib.mpcd_run(h, 0, 3, 0, st) == 0, lib.mpcd_last_error()
+            if a.split:  # per-kernel CUDA events inside mpcd_step (an extra timed run)
+                lib.mpcd_profile.argtypes = [C.c_void_p, C.c_int32]
+                lib.mpcd_read_profile.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+                lib.mpcd_profile(h, 1)
+                assert lib.mpcd_run(h, 3, 5, 0, st) == 0, lib.mpcd_last_error()
+                ms = (C.c_double * 5)()
+                ns = C.c_int64(0)
+                lib.mpcd_read_profile(h, ms, C.byref(ns))
+                lib.mpcd_profile(h, 0)
+                splits.setdefault(p, [round(ms[i] / max(ns.value, 1), 3) for i in range(3)])
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
@@ -82,6 +96,16 @@ def main():
             assert lib.mpcd_read_diag(h, C.byref(d), st) == 0
             assert d.n == n
             res[p].append(e0.elapsed_time(e1) / a.steps)
+            if r == 0 and a.hash:  # state after 3 + steps steps, id order: must agree across libs
+                import hashlib
+
+                import numpy as np
+                pos = np.empty((n, 3)); vel = np.empty((n, 3))
+                lib.mpcd_download.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_int32, C.c_void_p]
+                assert lib.mpcd_download(h, pos.ctypes.data, vel.ctypes.data, None, None, 1, st) == 0
+                torch.cuda.synchronize()
+                hashes[p] = hashlib.sha256(pos.tobytes() + vel.tobytes()).hexdigest()[:16]
             lib.mpcd_ctx_destroy(h)
             torch.cuda.empty_cache()
             os.environ.clear()
@@ -89,7 +113,10 @@ def main():
     for p in a.libs:
         v = res[p]
         print(json.dumps({"lib": p, "ms_per_step": sorted(v), "best": min(v),
-                          "gps": n / min(v) / 1e6}))
+                          "gps": n / min(v) / 1e6, "state": hashes.get(p),
+                          "k_step/dense/diag": splits.get(p)}))
+    if a.hash and len(set(hashes.values())) > 1:
+        print("STATE MISMATCH across libs:", hashes)
 
 
 if __name__ == "__main__":

@@ -66,3 +66,26 @@ for d in r.domains:
     print(f"domain {d.rank}: k_step {ms[0] / ns.value:.3f} ms, dense {ms[1] / ns.value:.3f}, "
           f"diag {ms[2] / ns.value:.3f} per step")
 r.close()
+
+# Weak-scaling form (BASELINE config 4 per GPU): a (2L) x L x L box as two
+# (2,1,1) domains of L^3 each, fused migration; each domain's k_step against
+# the whole L^3 box's k_step (same cells and particles per kernel).
+if os.environ.get("WEAK", "0") == "1":
+    r = SequentialRunner(mp.SimParams(edge_length=2 * L, edge_lengths=(2 * L, L, L), seed=0,
+                                      rank_dims=(2, 1, 1)),
+                         init="device")
+    for k in range(W):
+        r.advance(k, 0)
+    for d in r.domains:
+        lib.mpcd_profile(d.ctx.handle, 1)
+    for k in range(W, W + 10):
+        r.advance(k, 0)
+    d0 = r.run_step(W + 10)
+    for d in r.domains:
+        ms = (C.c_double * 5)()
+        ns = C.c_int64(0)
+        lib.mpcd_read_profile(d.ctx.handle, ms, C.byref(ns))
+        print(f"weak: domain {d.rank} of (2L,L,L), L={L}: k_step {ms[0] / ns.value:.3f} ms, "
+              f"dense {ms[1] / ns.value:.3f}, diag {ms[2] / ns.value:.3f} per step; "
+              f"{d0['crossings']} particles migrate/step")
+    r.close()
