@@ -22,6 +22,9 @@ int64_t launch_mode_multi(const StepArgs& A, int64_t nt, Variant v, int which, c
 int64_t launch_mode_fused(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st);
 
 constexpr int64_t kDenseGrid = 592;
+#ifndef MPCD_FIXTC
+#define MPCD_FIXTC 16
+#endif
 
 #ifdef MPCD_STEP_VARIANTS_ONLY
 namespace {
@@ -62,9 +65,10 @@ void allow_smem(const void* kernel, size_t smem) {
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE>
 int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_t st) {
   if (which == 0) {
-    // the 16-cell geometry compiled in, any other read at run time
-    auto kern = A.tc == 16 ? k_step<UNIT, UMASS, DRIFT, COM, MODE, 16>
-                           : k_step<UNIT, UMASS, DRIFT, COM, MODE, 0>;
+    // the common geometry (16 cells at ~10 particles per cell) compiled in,
+    // any other read at run time
+    auto kern = A.tc == MPCD_FIXTC ? k_step<UNIT, UMASS, DRIFT, COM, MODE, MPCD_FIXTC>
+                                   : k_step<UNIT, UMASS, DRIFT, COM, MODE, 0>;
     const size_t smem = sizeof(StepSmem<DRIFT>);
     const int64_t grid =
         std::max<int64_t>(1, std::min<int64_t>(ntiles, resident_ctas((const void*)kern, kNTW, smem)));

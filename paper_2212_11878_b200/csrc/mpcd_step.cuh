@@ -99,13 +99,6 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_SWZ_T
 #define MPCD_SWZ_T 0
 #endif
-// consumers (one-domain mode): the last pass of a tile parks its collided
-// records in their own tile slots and stores them one tile later, so the
-// slot claims' round trip overlaps the next tile's rank/moment phases; the
-// tile buffer is released after that flush
-#ifndef MPCD_DEFER
-#define MPCD_DEFER 0
-#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -694,6 +687,12 @@ __device__ __forceinline__ double pw_leaf_w(const double* base, int row0, int c,
 }
 // np.add.reduceat of column c over the k swizzled rows from row0 (k <= kSlotsW)
 __device__ __forceinline__ double reduceat_wcol(const double* base, int row0, int c, int k) {
+  if (!MPCD_SWZ_W) {  // immediate offsets; k <= kSlotsW < 130: one pairwise leaf
+    const double* t = base + row0 * 4 + c;
+    if (k <= 0) return 0.0;
+    if (k == 1) return t[0];
+    return t[0] + pw_leaf<4>(t + 4, k - 1);
+  }
   if (k <= 0) return 0.0;
   const double first = base[row0 * 4 + (c ^ (row_sw(row0) << 1))];
   if (k == 1) return first;
@@ -937,12 +936,14 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (0)
 #endif
 #if MPCD_AXPAIR
-  if (TILE_CELLS(A) <= 16 && A.prng == kSplitmix) {
+  if (A.prng == kSplitmix) {
     // two lanes per cell draw Marsaglia trials 2i and 2i + 1 at once (the
     // counter generator needs no sequential state); the first accepted
-    // trial in trial order wins, exactly as the one-lane loop
-    const int cell = lane >> 1, s = lane & 1;
-    const uint32_t ccnt = __shfl_sync(0xffffffffu, cnt, cell);
+    // trial in trial order wins, exactly as the one-lane loop.  16 cells
+    // per round of the warp.
+   for (int cg = 0; cg < TILE_CELLS(A); cg += 16) {
+    const int cell = cg + (lane >> 1), s = lane & 1;
+    const uint32_t ccnt = __shfl_sync(0xffffffffu, cnt, cell & 31);
     bool done = !(cell < TILE_CELLS(A) && ccnt > 0u);
     const uint64_t key = done ? 0ull : key_from_prefix(A.axis_prefix, global_cell_id<MODE>(A, c0 + cell));
     double* ax = B.ax + cell * 4;
@@ -970,6 +971,7 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
       }
     }
     if (!done && s == 0) atomicOr(&A.flags[1], 1u);  // 128 trials rejected
+   }
   } else
 #endif
   if (lane < kTC) {
@@ -982,50 +984,13 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane == 0) mbar_arrive(full);  // release: layout, table and axes written
 }
 
-// Stores a warp left pending (MPCD_DEFER): rows r with bit r of `mask` hold
-// a collided record parked in slot j0 + lane + 32 r of tile buffer `buf`,
-// bound for slot base[r] of next-step cell key[r].
-template <int R>
-struct Deferred {
-  uint32_t key[R], base[R];
-  unsigned mask;  // this lane's rows
-  int j0;
-  int buf;        // tile buffer still held (-1: none)
-};
-
-// Store the parked records, then hand the tile buffer back to the producer.
-template <int R, class Smem>
-__device__ __forceinline__ void flush_deferred(const StepArgs& A, Smem& S, Deferred<R>& D) {
-  if (D.buf < 0) return;
-  const int lane = threadIdx.x & 31;
-  TileBuf& P = S.buf[D.buf];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    if ((D.mask >> r) & 1u) {
-      double2 p01, p23, v01, v23;
-      lds_row32(P.p, D.j0 + lane + 32 * r, p01, p23);
-      lds_row32(P.v, D.j0 + lane + 32 * r, v01, v23);
-      const double o[6] = {p01.x, p01.y, p23.x, v01.x, v01.y, v23.x};
-      finish_slot<false>(A, D.key[r], 0u, D.base[r], o, bits_id(p23.y), v23.y);
-    }
-  }
-  fence_proxy_async();  // the parked slots' generic writes precede the next TMA fill
-  __syncwarp();
-  if (lane == 0) mbar_arrive(&S.empty[D.buf]);
-  D.buf = -1;
-  D.mask = 0u;
-}
 
 // One consumer warp's cells of one tile: every phase, R slot rows per lane.
-// `defer` (one-domain mode, last pass of the tile): park the collided
-// records instead of storing them, into D; a pending D of the previous tile
-// is flushed after this pass's moments.
 template <int R, bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE, class Smem>
 __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBuf& T,
                                               WarpScratch& W, int64_t c0, int cw0,
                                               int ncw, int j0, int j1, double* acc,
-                                              uint32_t& ncoll, Deferred<R>& D, bool defer,
-                                              int tb) {
+                                              uint32_t& ncoll) {
   constexpr bool BYID = MODE == kById;
   const int lane = threadIdx.x & 31;
 #ifdef MPCD_TIMING
@@ -1125,7 +1090,6 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
-  if (MPCD_DEFER && MODE == kBinned) flush_deferred<R>(A, S, D);
   MPCD_PROBE(3);
 
   // phase 4: rotate (collision.py:289-306), stream + wrap (particles.py:62-67),
@@ -1251,25 +1215,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   }
   MPCD_PROBE(6);
 #endif
-  if (MPCD_DEFER && MODE == kBinned && defer) {
-    // park: each row's record in its own slot (read by this lane only)
-    unsigned mask = 0u;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (stay[r]) {
-        const int j = j0 + lane + 32 * r;
-        sts_row32(T.p, j, make_double2(o[r][0], o[r][1]),
-                  make_double2(o[r][2], id_bits(pid[r])));
-        sts_row32(T.v, j, make_double2(o[r][3], o[r][4]), make_double2(o[r][5], mm[r]));
-        D.key[r] = key[r];
-        D.base[r] = base[r];
-        mask |= 1u << r;
-      }
-    }
-    D.mask = mask;
-    D.j0 = j0;
-    D.buf = tb;
-  } else if (!BYID) {
+  if (!BYID) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (stay[r]) finish_slot<MODE == kFused>(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
@@ -1366,10 +1312,6 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
   // px py pz sum(m v^2) mass, particles collided, particles sent to other ranks
   double acc[kDiagCols] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   uint32_t ncoll = 0u;  // particles collided by this thread's cell lanes (acc[5])
-  Deferred<kRowsW> D;
-  D.buf = -1;
-  D.mask = 0u;
-  D.j0 = 0;
   int64_t tile = blockIdx.x;
   int b = 0;
   uint32_t ph = 0u;
@@ -1390,7 +1332,6 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
       ncw = (int)max((int64_t)0, min((int64_t)ncw, A.C - c0 - cw0));
     if (T.skip) ncw = 0;
     if (ncw == 0) {
-      if (MPCD_DEFER && MODE == kBinned) flush_deferred<kRowsW>(A, S, D);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[b]);
       continue;
@@ -1408,14 +1349,12 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
       }
       consume_cells<kRowsW, UNIT, UMASS, DRIFT, COM, MODE>(A, S, T, W, c0, g0, g1 - g0,
                                                            (int)T.off[g0], (int)T.off[g1], acc,
-                                                           ncoll, D, g1 == gend, b);
+                                                           ncoll);
       __syncwarp();  // W is rewritten by the next pass
       g0 = g1;
     }
-    // the tile buffer is free for the producer (after the deferred stores)
-    if (!(MPCD_DEFER && MODE == kBinned) && lane == 0) mbar_arrive(&S.empty[b]);
+    if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
   }
-  if (MPCD_DEFER && MODE == kBinned) flush_deferred<kRowsW>(A, S, D);
 #ifdef MPCD_TIMING
   if (lane < 10) atomicAdd(&g_phase_cycles[lane], S.tim[warp][lane]);
 #endif
