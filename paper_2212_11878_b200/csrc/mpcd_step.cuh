@@ -1038,13 +1038,17 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       if (0)
 #endif
       if (A.ids31) {
+        // a real row's cell has at least one group of four: do-while over a
+        // pointer (no index arithmetic or entry test per group)
+        const uint4* q = reinterpret_cast<const uint4*>(W.id + lo);
+        const uint4* const qe = reinterpret_cast<const uint4*>(W.id + hi);
 #pragma unroll 1
-        for (int s = lo; s < hi; s += 4) {
-          const uint4 w = *reinterpret_cast<const uint4*>(W.id + s);
+        do {
+          const uint4 w = *q++;
           // both below 2^31: w < me is the sign bit of w - me
           rank += ((w.x - me) >> 31) + ((w.y - me) >> 31) + ((w.z - me) >> 31) +
                   ((w.w - me) >> 31);
-        }
+        } while (q < qe);
       } else {
 #pragma unroll 1
         for (int s = lo; s < hi; s += 4) {
