@@ -710,6 +710,9 @@ StepArgs step_args(mpcd_ctx* c, int64_t step, bool by_id) {
   A.dense_row0 = kMainRows;
   (void)by_id;
   A.peers = c->p2p ? c->d_peers : nullptr;
+  A.n_ranks = c->multi ? (int)((int64_t)c->dom.rank_dims[0] * c->dom.rank_dims[1] *
+                               c->dom.rank_dims[2])
+                       : 1;
   A.out_set = b ^ 1;
   if (c->multi) {
     A.G0 = (int)c->dom.global_dims[0]; A.G1 = (int)c->dom.global_dims[1];
@@ -1433,6 +1436,9 @@ int install_peers(mpcd_ctx* c, const std::vector<PeerBufs>& tab) {
   const int64_t P = (int64_t)c->dom.rank_dims[0] * c->dom.rank_dims[1] * c->dom.rank_dims[2];
   if ((int64_t)tab.size() != P) return fail(MPCD_ERR_TOPOLOGY, "peer table has %d of %lld ranks",
                                             (int)tab.size(), (long long)P);
+  if (P > kMaxPeers)  // k_step keeps the peers' pointers in shared memory
+    return fail(MPCD_ERR_TOPOLOGY, "fused migration connects at most %d ranks (%lld here): "
+                "use the exchange", kMaxPeers, (long long)P);
   if (c->d_peers) cudaFree(c->d_peers);
   MPCD_CUDA(cudaMalloc(&c->d_peers, sizeof(PeerBufs) * P));
   MPCD_CUDA(cudaMemcpy(c->d_peers, tab.data(), sizeof(PeerBufs) * P, cudaMemcpyHostToDevice));

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <type_traits>
+
 #include "mpcd.h"
 #include "mpcd_math.cuh"
 

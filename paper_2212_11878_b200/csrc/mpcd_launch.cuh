@@ -69,7 +69,7 @@ int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_
     // any other read at run time
     auto kern = A.tc == MPCD_FIXTC ? k_step<UNIT, UMASS, DRIFT, COM, MODE, MPCD_FIXTC>
                                    : k_step<UNIT, UMASS, DRIFT, COM, MODE, 0>;
-    const size_t smem = sizeof(StepSmem<DRIFT>);
+    const size_t smem = sizeof(StepSmem<DRIFT, MODE == kFused>);
     const int64_t grid =
         std::max<int64_t>(1, std::min<int64_t>(ntiles, resident_ctas((const void*)kern, kNTW, smem)));
     kern<<<(unsigned)grid, kNTW, smem, st>>>(A, ntiles);
@@ -87,8 +87,10 @@ int64_t launch_variant(const StepArgs& A, int64_t ntiles, int which, cudaStream_
 template <int MODE>
 int64_t launch_mode_t(const StepArgs& A, int64_t nt, Variant v, int which, cudaStream_t st) {
 #ifdef MPCD_ONLY_MAIN
-  // tuning builds (tools/build_variants.py): the binned unit-mass variant alone
-  if constexpr (MODE == kBinned) return launch_variant<true, true, false, false, kBinned>(A, nt, which, st);
+  // tuning builds (tools/build_variants.py): the unit-mass variant of the
+  // binned and fused modes alone
+  if constexpr (MODE == kBinned || MODE == kFused)
+    return launch_variant<true, true, false, false, MODE>(A, nt, which, st);
   else return -1;
 #else
 #define MPCD_V(U, M, D, C) \

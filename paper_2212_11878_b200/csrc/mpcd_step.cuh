@@ -107,9 +107,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 // SYS: system scope, for the words that other GPUs claim in too (fused
 // migration: a peer's k_step adds to this domain's counts over NVLink, and
 // device-scope atomics of two GPUs are not atomic with respect to each other)
+#ifndef MPCD_ABL_DEVSCOPE
+#define MPCD_ABL_DEVSCOPE 0  // timing ablation only: device-scope local claims in fused mode
+#endif
 template <bool SYS = false>
 __device__ __forceinline__ uint32_t count_claim(uint32_t* p, uint32_t v) {
-  if (SYS) return atomicAdd_system(p, v);
+  if (SYS && !MPCD_ABL_DEVSCOPE) return atomicAdd_system(p, v);
   if (!MPCD_CNT_EVICT_LAST) return atomicAdd(p, v);
   uint32_t old;
   asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], %2, %3;"
@@ -216,6 +219,7 @@ struct StepArgs {
   unsigned long long* send_n;  // claimed per destination (may exceed send_cap)
   uint32_t send_cap;
   const PeerBufs* peers;       // non-null: fused migration over peer memory
+  int n_ranks;                 // fused: ranks of the decomposed box (<= kMaxPeers)
   int out_set;                 // region set the step writes (the same on every rank)
 };
 
@@ -349,6 +353,25 @@ static __device__ __noinline__ void fused_put(const PeerBufs* peers, int b, uint
     } else {
       atomicOr_system(&P.small[2], 1u);
     }
+  }
+}
+
+// A fused leaver whose owner's cell is full (claimed slot >= cap): the
+// owner's overflow list.  Out of line (rare).
+static __device__ __noinline__ void fused_overflow(const PeerBufs* peers, int b,
+                                                   uint32_t ovf_cap, int dest, uint32_t key,
+                                                   double x, double y, double z, uint32_t id,
+                                                   double vx, double vy, double vz, double m) {
+  const PeerBufs& P = peers[dest];
+  const uint32_t q = atomicAdd_system(&P.small[4 + b], 1u);
+  if (q < ovf_cap) {
+    st2(&P.ovf[b].p[q].x, x, y);
+    st2(&P.ovf[b].p[q].z, z, id_bits(id));
+    st2(&P.ovf[b].v[q].vx, vx, vy);
+    st2(&P.ovf[b].v[q].vz, vz, m);
+    P.ovf_cell[b][q] = key;
+  } else {
+    atomicOr_system(&P.small[2], 1u);
   }
 }
 
@@ -808,12 +831,30 @@ struct __align__(16) WarpScratch {
 #endif
 constexpr int kStages = MPCD_STAGES;  // tile buffers in flight per CTA
 
-template <bool DRIFT>
+// Fused migration: the next-step count / record arrays of every rank, for
+// the region set this step writes (copied from A.peers at kernel start), so
+// a leaver's claim and store pick their target with a select, in line.
+// Only the fused kernel carries it: 48 KB of shared memory per CTA is the
+// most that keeps the 200 KB carve-out (56 KB of L1), and a larger carve-out
+// measured 7 % slower.  More ranks than kMaxPeers use the exchange.
+constexpr int kMaxPeers = 16;
+struct PeerTable {
+  uint32_t* count[kMaxPeers];
+  PRec* p[kMaxPeers];
+  VRec* v[kMaxPeers];
+};
+struct NoPeerTable {};
+
+template <bool DRIFT, bool PEERS = false>
 struct StepSmem {
   TileBuf buf[kStages];
   WarpScratch w[kNCW];
+  typename std::conditional<PEERS, PeerTable, NoPeerTable>::type peer;
   double post[DRIFT ? kTC * 4 : 1];
   double red[kNCW * kDiagCols];
+#ifdef MPCD_SMEM_PAD  // tuning: extra shared memory per CTA (carve-out / L1 experiments)
+  unsigned char pad_[MPCD_SMEM_PAD];
+#endif
 #ifdef MPCD_TIMING
   unsigned long long tim[kNCW][10];
 #endif
@@ -1152,8 +1193,16 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       // the staging below and the next row's whole chain
       grp[r] = 0u;
       base[r] = 0u;
-      if (!BYID && j0 + 32 * r < j1)
-        claim_slot<MODE == kFused>(A, stay[r], key[r], grp[r], base[r]);
+      if constexpr (MODE == kFused) {
+        // local or remote, one system-scope claim per particle: the
+        // owner's next-step count, picked with a select
+        if (real[r]) {
+          uint32_t* const cnt = stay[r] ? A.count_out : S.peer.count[dest[r]];
+          base[r] = count_claim<true>(cnt + key[r], 1u);
+        }
+      } else if (!BYID && j0 + 32 * r < j1) {
+        claim_slot<false>(A, stay[r], key[r], grp[r], base[r]);
+      }
 #endif
       const double m = mm[r];
       const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
@@ -1164,7 +1213,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
           sts_row32w(W.val, row[r], make_double2(m * w[0], m * w[1]),
                      make_double2(m * w[2], m * ke));
       }
-      if (decomposed(MODE) && real[r] && !stay[r]) {
+      if (MODE == kMulti && real[r] && !stay[r]) {
         // a leaver: park its record in its own tile slot (dest in the pad
         // word) and its owner-local cell in W.id; flushed after the pass, so
         // the hot loop carries no copy of the sending code
@@ -1219,12 +1268,29 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   }
   MPCD_PROBE(6);
 #endif
-  if (!BYID) {
+  if constexpr (MODE == kFused) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (stay[r]) {
+        finish_slot<true>(A, key[r], 0u, base[r], o[r], pid[r], mm[r]);
+      } else if (real[r]) {  // a leaver: straight into its owner's cell, over peer memory
+        acc[6] += 1.0;
+        if (base[r] < A.cap) {
+          const Recs dst{S.peer.p[dest[r]], S.peer.v[dest[r]]};
+          store_rec(dst, (uint64_t)key[r] * A.cap + base[r], o[r][0], o[r][1], o[r][2], pid[r],
+                    o[r][3], o[r][4], o[r][5], mm[r]);
+        } else {
+          fused_overflow(A.peers, A.out_set, A.ovf_cap, dest[r], key[r], o[r][0], o[r][1],
+                         o[r][2], pid[r], o[r][3], o[r][4], o[r][5], mm[r]);
+        }
+      }
+    }
+  } else if (!BYID) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (stay[r]) finish_slot<MODE == kFused>(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
+      if (stay[r]) finish_slot<false>(A, key[r], grp[r], base[r], o[r], pid[r], mm[r]);
   }
-  if (decomposed(MODE) && __any_sync(0xffffffffu, leavers != 0u)) {
+  if (MODE == kMulti && __any_sync(0xffffffffu, leavers != 0u)) {
     // the pass's leavers, from their parked slots: one copy of the sending
     // code, run only by passes that have any
 #pragma unroll 1
@@ -1271,7 +1337,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
 template <bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE, int FIX>
 __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int64_t ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  StepSmem<DRIFT>& S = *reinterpret_cast<StepSmem<DRIFT>*>(smem_raw);
+  using Smem = StepSmem<DRIFT, MODE == kFused>;
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t G = gridDim.x;
 #ifdef MPCD_TIMING
@@ -1283,6 +1350,14 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
       mbar_init(&S.empty[b], kNCW);
     }
     fence_mbar_init();
+  }
+  if constexpr (MODE == kFused) {
+    if (t < A.n_ranks) {
+      const PeerBufs& P = A.peers[t];
+      S.peer.count[t] = P.count[A.out_set];
+      S.peer.p[t] = P.reg[A.out_set].p;
+      S.peer.v[t] = P.reg[A.out_set].v;
+    }
   }
   __syncthreads();
 
