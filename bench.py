@@ -156,6 +156,87 @@ class ClockSampler:
                 "samples": len(rows), "samples_under_load": len(loaded)}
 
 
+class NvmlClockSampler:
+    """SM clocks and clock-event (throttle) reasons polled through NVML every
+    ~2 ms by a thread during the timed region, so even a 20-step region of
+    ~130 ms yields tens of samples (nvidia-smi's 50 ms loop yielded 2).
+    Falls back to ClockSampler (nvidia-smi) when NVML is unavailable."""
+
+    # nvmlClocksEventReason* bits (nvml.h)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index, period=0.002):
+        self.index = index
+        self.period = period
+        self.rows = []
+        self.ok = False
+        self.fallback = None
+
+    def _handle(self, nv):
+        import torch
+
+        try:  # the NVML device of this CUDA ordinal (CUDA_VISIBLE_DEVICES may remap)
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            if not uuid.startswith("GPU-"):
+                uuid = "GPU-" + uuid
+            return nv.nvmlDeviceGetHandleByUUID(uuid.encode())
+        except Exception:  # noqa: BLE001
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self):
+        nv, h = self.nv, self.h
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h) \
+                    if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((sm, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        import threading
+
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = self._handle(nv)
+            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 -- no NVML: nvidia-smi
+            self.fallback = ClockSampler(self.index).__enter__()
+            return self
+        self.stop = False
+        self.thread = threading.Thread(target=self._poll, daemon=True)
+        self.thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.fallback is not None:
+            return self.fallback.__exit__(*exc)
+        if self.ok:
+            self.stop = True
+            self.thread.join(timeout=5)
+        return False
+
+    def summary(self):
+        if self.fallback is not None:
+            return self.fallback.summary()
+        rows = list(self.rows)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm if self.ok else None,
+                    "reasons": ["unsampled"]}
+        reasons = sorted({n for _, rs in rows for n, b in self.BITS.items() if rs & b})
+        return {"sm_mhz": statistics.median(sm for sm, _ in rows), "sm_max_mhz": self.max_sm,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(rows),
+                "sampler": f"NVML every {self.period * 1e3:g} ms during the timed region"}
+
+
 def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -265,9 +346,10 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / timed, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (oracle init_system)",
-        "config": {"workload": workload_text(args, 1, None),
-                   "cells_per_gpu": L ** 3, "particles_per_gpu": n, "parallelism": "cpu",
-                   "steps_timed": timed},
+        "config": config_of(args, ws, workload_params(args, ws)),
+        "layout": f"CPU reference on the host: {L}^3 cells x 10 per timed step "
+                  f"({timed} timed steps)" + ("" if ws == 1 else
+                  f"; the GPU arm's per-GPU share of the {ws}-GPU box is {L}^3 cells x 10"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -356,7 +438,7 @@ def run_ours(args):
 
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with NvmlClockSampler(local) as clocks:
         barrier()
         torch.cuda.synchronize()
         start.record(stream)
@@ -408,9 +490,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (device init_system: uniform positions, N(0,1) velocities minus "
                 "their mean, unit masses)",
-        "config": {"workload": workload_text(args, ws, params),
-                   "cells_per_gpu": C, "particles_per_gpu": n,
-                   "parallelism": "single domain" if ws == 1 else
+        "config": config_of(args, ws, params),
+        "layout": {"parallelism": "single domain" if ws == 1 else
                    f"{'slab' if params.rank_dims[1:] == (1, 1) else 'pencil'} decomposition "
                    f"{tuple(params.rank_dims)} of a {'x'.join(map(str, params.dims))} box, "
                    "particle migration every step: " +
@@ -418,7 +499,7 @@ def run_ours(args):
                     ("gloo barrier step fence (host-staged check mode)" if exch.host_staged
                      else "NCCL all-reduce step fence")
                     if fused else "send buffers + point-to-point exchange"),
-                   "l2": "state 17 GB >> 126 MB L2; no flush needed"},
+                   "l2": "state 17 GB >> 126 MB L2 per GPU; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": survey_launch,
@@ -428,7 +509,13 @@ def run_ours(args):
                      "b_min_frac": B_MIN_N * n / (per_kernel[top] * 1e-3) / 1e9 / peak,
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, "
                                        "dram__bytes_read.sum + dram__bytes_write.sum)",
-                     "avg_launch_ms": per_kernel[top], "peak_source": peak_src},
+                     "avg_launch_ms": per_kernel[top], "peak_source": peak_src,
+                     # the DRAM bytes ncu measured for one launch, over this run's
+                     # launch time: the fraction of the copy peak the kernel
+                     # actually moves (the survey-byte `frac` counts bytes this
+                     # one-pass design never moves)
+                     "dram_frac": (traffic / (per_kernel[top] * 1e-3) / 1e9 / peak)
+                     if traffic else None},
         "roofline_step": {
             "bytes_per_step": step_bytes, "achieved": step_bytes / (ms * 1e-3) / 1e9,
             "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
@@ -462,6 +549,32 @@ def run_ours(args):
     ctx.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def workload_params(args, ws):
+    """The SimParams of the workload both arms describe (config 3 at N = 1,
+    config 4 / 5 at N > 1)."""
+    from paper_2212_11878_b200.params import SimParams
+
+    L = args.L
+    if ws == 1:
+        return SimParams(edge_length=L, seed=args.seed)
+    if args.config == 5:
+        dims = (1024, 512, 512)
+        rank_dims = {8: (4, 2, 1), 16: (4, 2, 2)}.get(ws)
+        if rank_dims is None:
+            raise SystemExit("config 5 needs 8 GPUs (1.1 TB of cell regions)")
+    else:
+        dims, rank_dims = (L * ws, L, L), (ws, 1, 1)
+    return SimParams(edge_length=dims[0], edge_lengths=dims, seed=args.seed, rank_dims=rank_dims)
+
+
+def config_of(args, ws, params):
+    """`config` of the JSON line: identical for our arm and the reference arm
+    (the driver compares them); how each arm runs it is reported outside."""
+    cells = params.dims[0] * params.dims[1] * params.dims[2]
+    return {"workload": workload_text(args, ws, params), "cells_per_gpu": cells // ws,
+            "particles_per_gpu": params.n_particles // ws}
 
 
 def workload_text(args, ws, params):
