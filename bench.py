@@ -288,8 +288,13 @@ def reference_package_cases(seed):
     while ranks * 2 <= min(cpus, 64):
         ranks *= 2
     out = {}
-    for name, backend, nranks in (("serial_64", "serial", 1), ("process_64", "process", ranks)):
-        params = RParams(edge_length=64, mean_density=PPC, dt=0.1, alpha=math.radians(130.0),
+    # serial on 1 core at 16^3 and 64^3, process on all cores;
+    # the process backend runs at 64^3 and 128^3 (256^3 needs ~46 GB of host
+    # RAM and minutes per step in numpy, beyond the reference arm's budget)
+    cases = (("serial_16", "serial", 1, 16), ("serial_64", "serial", 1, 64),
+             ("process_64", "process", ranks, 64), ("process_128", "process", ranks, 128))
+    for name, backend, nranks, L in cases:
+        params = RParams(edge_length=L, mean_density=PPC, dt=0.1, alpha=math.radians(130.0),
                          seed=seed, n_steps=3, rank_dims=rbench.rank_dims_for(nranks))
         t0 = time.perf_counter()
         rec = rbench.run_benchmark_case(params, steps=2, warmup=1, backend=backend)
@@ -297,7 +302,8 @@ def reference_package_cases(seed):
         out[name] = {"value": rec.particles * rec.steps / rec.seconds, "unit": UNIT,
                      "cores": nranks, "backend": backend, "ranks": list(params.rank_dims),
                      "seconds_per_step": rec.seconds / rec.steps, "wall_s": wall,
-                     "sample": "64^3 x 10 (2,621,440 particles), 1 warm-up + 2 timed steps"}
+                     "sample": f"{L}^3 x 10 ({L ** 3 * 10:,} particles), 1 warm-up + 2 timed "
+                               "steps, mpcdsim.bench.run_benchmark_case"}
     return out
 
 
@@ -305,7 +311,7 @@ def run_reference(args):
     """The reference's CPU implementation of the step on this host's cores
     (the oracle: the reference algorithm restated in C, bit-exact with it,
     all host threads) on the SAME workload as our arm -- args.L^3 cells x 10
-    -- with warm-up capped at 2 steps and the timed steps capped at ~240 s of
+    -- with warm-up capped at 2 steps and the timed steps capped at ~120 s of
     host work (the metric is a rate).  The reference package's own benchmark
     runs beside it when installed (reference_package_cases)."""
     ws, rank, _ = dist_setup(args)
@@ -329,7 +335,7 @@ def run_reference(args):
         pos, vel = r.positions, r.velocities
     timed = args.steps
     if t_warm:
-        timed = max(1, min(args.steps, int(240.0 / t_warm)))
+        timed = max(1, min(args.steps, int(120.0 / t_warm)))
     t0 = time.perf_counter()
     for k in range(warm, warm + timed):
         r = oracle.serial_step(pos, vel, mass, L, 1.0, 0.1, cs, sn, args.seed, k)
@@ -338,7 +344,7 @@ def run_reference(args):
     del pos, vel, r
     value = n * timed / dt
     sample = (f"{L}^3 cells x 10 ({n} particles) per step -- the benchmark workload itself -- "
-              f"{warm} warm-up + {timed} timed steps of the {args.steps} asked (capped at ~240 s "
+              f"{warm} warm-up + {timed} timed steps of the {args.steps} asked (capped at ~120 s "
               f"of host work), {threads} OpenMP threads, oracle/mpcd_oracle.c (the reference "
               "algorithm restated in C, bit-exact with the reference package)")
     line = {
