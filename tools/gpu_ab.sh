@@ -1,4 +1,3 @@
 set -x
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench20.log 2>&1; tail -1 gpurun_out/bench20.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['value'], l['ms_per_step'], l['clocks'], l['roofline']['dram_frac'], l['config'])"
-MPCD_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --L 64 --steps 5 --warmup 3 > gpurun_out/bench_2rank.log 2>&1; tail -1 gpurun_out/bench_2rank.log | cut -c1-700
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --L 64 --steps 2 --warmup 1 > gpurun_out/bench_ref_2rank.log 2>&1; tail -1 gpurun_out/bench_ref_2rank.log | cut -c1-400
+timeout 900 python tools/pcie_probe.py 2>&1 | tail -8
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_density.py -q -x 2>&1 | tail -3
