@@ -391,3 +391,28 @@ def test_two_gpus_nccl_equal_whole_box(tmp_path, L, steps, migration):
     for o in parts:
         assert str(o["used"]) == migration
         assert np.all(o["crossings"] > 0)
+
+
+def test_ids_above_2_31_rank_with_unsigned_compares():
+    """Global ids above 2^31 - 1 (a system of more than 2^31 particles, e.g.
+    BASELINE config 5's 2.7 G) switch k_step's in-cell ranking from the
+    sign-bit compare to the unsigned compare.  Ids 3e9 + i order like i, so
+    the decomposed box must equal the whole box (ids i) bit for bit."""
+    from paper_2212_11878_b200.distributed import SequentialRunner
+
+    base = mp.SimParams(edge_length=16, seed=31)
+    ids_w, p_w, _, _, _ = run(base, "cuda", 3)
+    p0 = mp.init_system(base)
+    big = np.int64(3_000_000_000) + np.arange(p0.n, dtype=np.int64)
+    r = SequentialRunner(mp.SimParams(edge_length=16, seed=31, rank_dims=(2, 1, 1)))
+    try:
+        for d in r.domains:  # every domain takes the whole box's rows and keeps its own
+            d.ctx.upload(p0.positions, p0.velocities, None, big, 0)
+        for k in range(3):
+            r.run_step(k)
+        ids, p = r.collect()
+    finally:
+        r.close()
+    assert np.array_equal(ids, big)
+    assert np.array_equal(p.positions, p_w.positions)
+    assert np.array_equal(p.velocities, p_w.velocities)
