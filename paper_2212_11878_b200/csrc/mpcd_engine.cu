@@ -948,9 +948,10 @@ int mpcd_ctx_create(const mpcd_config* cfg, mpcd_ctx** out) {
     const double regions = 2.0 * (double)C * cap * 64.0;
     const double spare = (double)free_b - regions - 4.0 * (1ull << 30);
     int shift = 2;  // n / 4 overflow entries, n / 2 staged rows
-    // per particle of overflow capacity: 2 lists x (64 B record + 4 B cell) +
-    // 4 B bucket index; of staging: 40 B
-    while (shift < 4 && spare < (double)cap_n * (140.0 / (1 << shift) + 40.0 / (2 << shift)))
+    // per particle of overflow capacity (n >> shift entries): 2 lists x (64 B
+    // record + 4 B cell) + 4 B bucket index; of staging (n >> (shift - 1)
+    // rows): 40 B
+    while (shift < 4 && spare < (double)cap_n * (140.0 / (1 << shift) + 40.0 / (1 << (shift - 1))))
       ++shift;
     c->ovf_cap = (uint32_t)std::min<int64_t>(cap_n, std::max<int64_t>(cap_n >> shift, 1 << 16));
     c->scratch_cap =
