@@ -153,8 +153,11 @@ int mpcd_step_host(mpcd_ctx* ctx, double* pos, double* vel, const double* mass, 
 /* Out-of-place form of mpcd_step_host: reads pos_in/vel_in, writes the
  * stepped rows (input order) to pos_out/vel_out (which may alias the
  * inputs).  Page-locked buffers (mpcd_host_alloc, cudaHostAlloc/Register)
- * are read and written in place by the kernels over PCIe; pageable ones are
- * staged through device memory. */
+ * move by DMA in 8 Mi-row chunks on a copy stream, each chunk binned (input)
+ * or produced (output) by a kernel while the next is in flight; below 2 Mi
+ * rows the kernels read and write them in place over PCIe.  Pageable
+ * buffers are staged through device memory.  Returns after the output rows
+ * are on the host. */
 int mpcd_step_rows(mpcd_ctx* ctx, const double* pos_in, const double* vel_in, const double* mass,
                    int64_t n, int64_t step, int32_t flags, double* pos_out, double* vel_out,
                    double* drift, void* stream);
