@@ -237,7 +237,10 @@ int mpcd_absorb(mpcd_ctx* ctx, const void* recs, int64_t n_recv, int64_t n_sent,
  * mpcd_ipc_handles exports this context's region / count / overflow
  * allocations as CUDA IPC handles (*nbytes bytes; out = NULL asks the size);
  * mpcd_connect_peers takes every rank's handles concatenated in rank order
- * and opens the others'.  Domains of one process (one GPU or several)
+ * and opens the others'.  Each rank's blob ends with its domain geometry
+ * (cells, slots per cell, overflow capacity); connecting requires equal
+ * geometry on every rank (else MPCD_ERR_TOPOLOGY, nothing opened: use the
+ * exchange).  Domains of one process (one GPU or several)
  * connect directly with mpcd_connect_local(ctxs[rank], n). */
 int mpcd_ipc_handles(mpcd_ctx* ctx, void* out, int64_t* nbytes);
 int mpcd_connect_peers(mpcd_ctx* ctx, const void* all_handles, int32_t n_ranks);

@@ -1563,10 +1563,21 @@ int install_peers(mpcd_ctx* c, const std::vector<PeerBufs>& tab) {
 }
 }  // namespace
 
+// Each rank's blob: its allocations' IPC handles, then the geometry a peer
+// addresses them with (cells, slots per cell, overflow capacity).  A peer's
+// k_step indexes the owner's regions and overflow list with its own values,
+// so connecting requires equal geometry (the overflow capacity follows the
+// free device memory at context creation and could differ between GPUs).
+struct IpcGeometry {
+  int64_t C, cap, ovf_cap;
+};
+constexpr int64_t kIpcBlob = kIpcAllocs * (int64_t)sizeof(cudaIpcMemHandle_t) +
+                             (int64_t)sizeof(IpcGeometry);
+
 int mpcd_ipc_handles(mpcd_ctx* c, void* out, int64_t* nbytes) {
   clear_error();
   if (!c || !nbytes) return fail(MPCD_ERR_CONFIG, "null argument");
-  const int64_t need = kIpcAllocs * (int64_t)sizeof(cudaIpcMemHandle_t);
+  const int64_t need = kIpcBlob;
   if (!out) {
     *nbytes = need;
     return MPCD_OK;
@@ -1577,6 +1588,8 @@ int mpcd_ipc_handles(mpcd_ctx* c, void* out, int64_t* nbytes) {
                               c->ovf_slab[1], c->ovf_cell[0], c->ovf_cell[1], c->small};
   cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(out);
   for (int i = 0; i < kIpcAllocs; ++i) MPCD_CUDA(cudaIpcGetMemHandle(&h[i], allocs[i]));
+  const IpcGeometry g{c->C, (int64_t)c->cap, (int64_t)c->ovf_cap};
+  memcpy(h + kIpcAllocs, &g, sizeof(g));
   *nbytes = need;
   return MPCD_OK;
 }
@@ -1586,18 +1599,28 @@ int mpcd_connect_peers(mpcd_ctx* c, const void* all, int32_t n_ranks) {
   if (!c || !all) return fail(MPCD_ERR_CONFIG, "null argument");
   if (!c->multi) return fail(MPCD_ERR_CONFIG, "not a decomposed domain (mpcd_ctx_set_domain)");
   DeviceGuard dg(c->dev);
-  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all);
+  const char* blobs = static_cast<const char*>(all);
   const uint64_t rows = (uint64_t)c->C * c->cap, orows = c->ovf_cap;
+  for (int r = 0; r < n_ranks; ++r) {  // equal geometry first: nothing opened on failure
+    IpcGeometry g;
+    memcpy(&g, blobs + r * kIpcBlob + kIpcAllocs * sizeof(cudaIpcMemHandle_t), sizeof(g));
+    if (g.C != c->C || g.cap != (int64_t)c->cap || g.ovf_cap != (int64_t)c->ovf_cap)
+      return fail(MPCD_ERR_TOPOLOGY,
+                  "rank %d's domain differs (cells %lld, cap %lld, overflow %lld; here %lld, "
+                  "%u, %u): fused migration needs equal geometry",
+                  r, (long long)g.C, (long long)g.cap, (long long)g.ovf_cap, (long long)c->C,
+                  c->cap, c->ovf_cap);
+  }
   std::vector<PeerBufs> tab(n_ranks);
   for (int r = 0; r < n_ranks; ++r) {
     if (r == c->dom.rank) {
       tab[r] = local_bufs(c);
       continue;
     }
+    const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(blobs + r * kIpcBlob);
     void* p[kIpcAllocs];
     for (int i = 0; i < kIpcAllocs; ++i) {
-      MPCD_CUDA(cudaIpcOpenMemHandle(&p[i], h[r * kIpcAllocs + i],
-                                     cudaIpcMemLazyEnablePeerAccess));
+      MPCD_CUDA(cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess));
       c->ipc_opened.push_back(p[i]);
     }
     // every rank has the same cells per domain, cap and overflow capacity

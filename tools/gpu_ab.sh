@@ -1,3 +1,2 @@
 set -x
-V=build/variants
-timeout 900 python tools/ab_time.py $V/base2.so $V/ldg.so --rounds 3 --steps 20 2>&1 | tail -3
+timeout 1200 python -m pytest tests/test_gpu_distributed.py -q -x 2>&1 | tail -3
