@@ -401,7 +401,7 @@ __device__ __forceinline__ bool next_cell_multi(const StepArgs& A, double x, dou
     gz = cell_coord32<UNIT>(z, A.off_next2, A.a, A.G2);
   }
   const unsigned lx = (unsigned)(gx - A.o0), ly = (unsigned)(gy - A.o1), lz = (unsigned)(gz - A.o2);
-  if (lx < (unsigned)A.L0 && ly < (unsigned)A.L1 && lz < (unsigned)A.L2) {
+  if (__builtin_expect((lx < (unsigned)A.L0) & (ly < (unsigned)A.L1) & (lz < (unsigned)A.L2), 1)) {
     key = (lx * (unsigned)A.L1 + ly) * (unsigned)A.L2 + lz;
     return true;
   }
@@ -1197,7 +1197,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
         // local or remote, one system-scope claim per particle: the
         // owner's next-step count, picked with a select
         if (real[r]) {
-          uint32_t* const cnt = stay[r] ? A.count_out : S.peer.count[dest[r]];
+          uint32_t* cnt = A.count_out;
+          if (__builtin_expect(!stay[r], 0)) cnt = S.peer.count[dest[r]];
           base[r] = count_claim<true>(cnt + key[r], 1u);
         }
       } else if (!BYID && j0 + 32 * r < j1) {
@@ -1273,9 +1274,9 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     for (int r = 0; r < R; ++r) {
       if (stay[r]) {
         finish_slot<true>(A, key[r], 0u, base[r], o[r], pid[r], mm[r]);
-      } else if (real[r]) {  // a leaver: straight into its owner's cell, over peer memory
+      } else if (__builtin_expect(real[r], 0)) {  // a leaver: into its owner's cell, over peer memory
         acc[6] += 1.0;
-        if (base[r] < A.cap) {
+        if (__builtin_expect(base[r] < A.cap, 1)) {
           const Recs dst{S.peer.p[dest[r]], S.peer.v[dest[r]]};
           store_rec(dst, (uint64_t)key[r] * A.cap + base[r], o[r][0], o[r][1], o[r][2], pid[r],
                     o[r][3], o[r][4], o[r][5], mm[r]);
