@@ -5,6 +5,7 @@ Run on a B200: python -m pytest tests -m gpu
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -495,6 +496,37 @@ def test_public_pure_step_zero_copy_chain():
     pm = mp.ParticleSet(p0.positions, p0.velocities, m)
     out, _, _ = mp.serial_collision_step(pm, params, 0)
     r = oracle.serial_step(p0.positions, p0.velocities, m, 12, 1.0, params.dt, cs, sn,
+                           params.seed, 0)
+    assert np.array_equal(out.positions, r.positions)
+    assert np.array_equal(out.velocities, r.velocities)
+
+
+def test_public_pure_step_pipelined_transfers():
+    """Above 2 Mi rows the pure function moves pinned rows by chunked DMA (8 Mi
+    rows per chunk, each binned / produced by a kernel on arrival) and checks
+    the masses on a worker thread while the GPU steps with the first mass as
+    its guess.  104^3 x 10 = 11.2 M rows: a full chunk plus a partial one;
+    uniform masses, then non-uniform ones (the guess fails and the
+    per-particle-mass path runs): the oracle's steps bit for bit."""
+    params = mp.SimParams(edge_length=104, seed=5)
+    p0 = mp.init_system(params)
+    n = p0.n
+    assert n > (1 << 23)
+    oracle.set_threads(os.cpu_count() or 1)
+    cs, sn = float(np.cos(params.alpha)), float(np.sin(params.alpha))
+    q = p0
+    ref_pos, ref_vel = p0.positions, p0.velocities
+    for k in range(2):
+        q, _, _ = mp.serial_collision_step(q, params, k)
+        r = oracle.serial_step(ref_pos, ref_vel, np.ones(n), 104, 1.0, params.dt, cs, sn,
+                               params.seed, k)
+        ref_pos, ref_vel = r.positions, r.velocities
+        assert np.array_equal(q.positions, ref_pos) and np.array_equal(q.velocities, ref_vel), k
+    m = np.ones(n)
+    m[n - 3] = 1.5  # the first mass is a wrong guess only at the very end
+    out, _, _ = mp.serial_collision_step(mp.ParticleSet(p0.positions, p0.velocities, m),
+                                         params, 0)
+    r = oracle.serial_step(p0.positions, p0.velocities, m, 104, 1.0, params.dt, cs, sn,
                            params.seed, 0)
     assert np.array_equal(out.positions, r.positions)
     assert np.array_equal(out.velocities, r.velocities)
