@@ -767,6 +767,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 
 #ifdef MPCD_TIMING
 static __device__ unsigned long long g_phase_cycles[10];
+// producer warps: [0] cycles waiting for a free buffer, [1] cycles preparing tiles
+static __device__ unsigned long long g_prod_cycles[2];
 // per-warp shared accumulators (S.tim), flushed once per warp at kernel end
 #define MPCD_PROBE(k)                                                              \
   do {                                                                             \
@@ -1373,16 +1375,35 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
     // no 64-bit division per tile
     int b = 0;
     uint32_t ph = 0u;
+#ifdef MPCD_TIMING
+    unsigned long long pw = 0ull, pp = 0ull;
+#endif
     for (int64_t i = 0; tile < ntiles; ++i, tile += G) {
       const uint32_t cnt_next = tile_count<FIX>(A, tile + G, ntiles);  // in flight meanwhile
+#ifdef MPCD_TIMING
+      const long long q0 = clock64();
+#endif
       if (i >= kStages) mbar_wait(&S.empty[b], ph ^ 1u);
+#ifdef MPCD_TIMING
+      const long long q1 = clock64();
+#endif
       prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
+#ifdef MPCD_TIMING
+      pw += (unsigned long long)(q1 - q0);
+      pp += (unsigned long long)(clock64() - q1);
+#endif
       cnt = cnt_next;
       if (++b == kStages) {
         b = 0;
         ph ^= 1u;
       }
     }
+#ifdef MPCD_TIMING
+    if (lane == 0) {
+      atomicAdd(&g_prod_cycles[0], pw);
+      atomicAdd(&g_prod_cycles[1], pp);
+    }
+#endif
     return;
   }
 

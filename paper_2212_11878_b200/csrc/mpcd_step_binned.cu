@@ -19,11 +19,14 @@ int64_t launch_mode_binned(const StepArgs& A, int64_t nt, Variant v, int which, 
 // consumer warps of this translation unit's kernels (tools/phase_timing.py).
 extern "C" int mpcd_debug_phase_cycles(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, mpcd::g_phase_cycles, sizeof(unsigned long long) * 10) !=
+      cudaSuccess ||
+      cudaMemcpyFromSymbol(out + 10, mpcd::g_prod_cycles, sizeof(unsigned long long) * 2) !=
       cudaSuccess)
     return MPCD_ERR_CUDA;
   if (reset) {
     unsigned long long z[10] = {0};
     cudaMemcpyToSymbol(mpcd::g_phase_cycles, z, sizeof(z));
+    cudaMemcpyToSymbol(mpcd::g_prod_cycles, z, 2 * sizeof(unsigned long long));
   }
   return MPCD_OK;
 }

@@ -1,2 +1,2 @@
 set -x
-timeout 1200 python -m pytest tests/test_gpu_distributed.py -q -x 2>&1 | tail -3
+MPCD_LIB=build/variants/timing.so timeout 600 python tools/phase_timing.py 256 2>&1 | tail -12

@@ -1,4 +1,5 @@
-# Round-2 evidence run: GPU tests, smoke, bench (both arms), launch list, one ncu capture, density sweep
+# Round-2 evidence run: GPU tests, smoke, bench (both arms), launch list, one ncu capture,
+# density sweep, memcheck of the dense / cluster cases
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
@@ -8,5 +9,5 @@ timeout 900 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/benc
 timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1; tail -1 gpurun_out/bench_reference.log | cut -c1-600
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 2 -c 1 -o gpurun_out/k_step_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-timeout 900 python tools/density_sweep.py --out gpurun_out/density_sweep.json > gpurun_out/density_sweep.log 2>&1; tail -3 gpurun_out/density_sweep.log
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_density.py > gpurun_out/sanitize_memcheck.log 2>&1; tail -3 gpurun_out/sanitize_memcheck.log
 ls -la gpurun_out

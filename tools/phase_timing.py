@@ -21,7 +21,7 @@ ctx.init_device(p.n_particles, 1.0, 0)
 ctx.run(0, 3)
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (C.c_ulonglong * 10)()
+buf = (C.c_ulonglong * 12)()
 lib.mpcd_debug_phase_cycles(buf, 1)
 steps = 5
 ctx.run(3, steps)
@@ -35,3 +35,8 @@ tot = sum(v[1:9])
 print(f"L={L}: {tiles} warp-tile visits over {steps} steps")
 for k in range(1, 9):
     print(f"  {names[k]:22s} {v[k] / max(tiles, 1):9.1f} cycles/warp-tile  {100 * v[k] / tot:5.1f} %")
+
+tiles_p = tiles / 4  # one producer per 4 consumer warps
+print(f"  producer: waiting for a free buffer {v[10] / max(tiles_p, 1):9.1f} cycles/tile, "
+      f"preparing {v[11] / max(tiles_p, 1):9.1f} cycles/tile "
+      f"({100 * v[10] / max(v[10] + v[11], 1):.1f} % waiting)")
