@@ -416,3 +416,55 @@ def test_ids_above_2_31_rank_with_unsigned_compares():
     assert np.array_equal(ids, big)
     assert np.array_equal(p.positions, p_w.positions)
     assert np.array_equal(p.velocities, p_w.velocities)
+
+
+def _geometry_worker(rank, world, port, out_dir):
+    import warnings
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2212_11878_b200.distributed import (CudaDomain, DistExchange, DomainLayout,
+                                                   _DomainRunner, connect_fused)
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        params = mp.SimParams(edge_length=16, seed=7, rank_dims=(world, 1, 1))
+        layout = DomainLayout.from_params(params)
+        # rank 1 sizes its context larger: its cell capacity (and overflow
+        # list) differ from rank 0's, so the fused connection must refuse
+        cap = 30_000 if rank == 0 else 200_000
+        dom = CudaDomain(params, layout, rank, capacity=cap)
+        exch = DistExchange()
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            fused = connect_fused(dom, exch)
+        dom.upload(mp.init_system(mp.SimParams(edge_length=16, seed=7)))
+        runner = _DomainRunner(params, [dom], exch, capture_drift=False, capture_com=False,
+                               fused=fused)
+        for k in range(3):
+            runner.run_step(k)
+        ids, p = runner.collect()
+        np.savez(os.path.join(out_dir, f"g{rank}.npz"), ids=ids, pos=p.positions,
+                 vel=p.velocities, fused=fused, warned=any("fused" in str(x.message) for x in w))
+        runner.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_connection_refuses_unequal_geometry(tmp_path):
+    """Two ranks whose contexts differ in slots per cell: mpcd_connect_peers
+    rejects the connection (a peer would address the other's regions with
+    the wrong stride), connect_fused warns and every rank falls back to the
+    exchange, and the result is still the whole box bit for bit."""
+    import torch.multiprocessing as tmp_mp
+
+    tmp_mp.spawn(_geometry_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    ids, p, _, _, _ = run(mp.SimParams(edge_length=16, seed=7), "cuda", 3)
+    for r in range(2):
+        o = np.load(tmp_path / f"g{r}.npz")
+        assert not bool(o["fused"]) and bool(o["warned"])
+        assert np.array_equal(o["ids"], ids)
+        assert np.array_equal(o["pos"], p.positions)
+        assert np.array_equal(o["vel"], p.velocities)
