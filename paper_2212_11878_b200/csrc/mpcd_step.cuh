@@ -93,6 +93,11 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 // (measured slower on B200: the kernel's time follows its instruction count,
 // and the swizzles' selects / column index math cost more issue slots than
 // the bank conflicts they remove -- profiles/r02_k_step.md)
+// producer: draw the next tile's axes into registers before waiting for a
+// free buffer (the draw's latency hides in the wait)
+#ifndef MPCD_EARLYAX
+#define MPCD_EARLYAX 1
+#endif
 #ifndef MPCD_SWZ_W
 #define MPCD_SWZ_W 0
 #endif
@@ -883,13 +888,59 @@ __device__ __forceinline__ uint32_t tile_count(const StepArgs& A, int64_t tl, in
   return (lane < TILE_CELLS(A) && tl < ntiles && c < A.C) ? __ldcg(A.count_in + c) : 0u;
 }
 
+// A tile's rotation axes drawn ahead into registers (tiles of <= 16 cells,
+// the reference's counter generator): lane pair (2 c, 2 c + 1) draws cell c;
+// `write` marks the lane that stores B.ax[c] (the winning lane of the pair,
+// or lane 2 c for an empty cell, whose axis stays zero).
+struct AxisReg {
+  double a0, a1, a2;
+  bool write;
+};
+
+template <int MODE, int FIX>
+__device__ __forceinline__ AxisReg draw_axes_early(const StepArgs& A, int64_t tl,
+                                                   int64_t ntiles, uint32_t cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = tl * TILE_CELLS(A);
+  const int nc = tl < ntiles ? (int)min((int64_t)TILE_CELLS(A), A.C - c0) : 0;
+  const int cell = lane >> 1, s = lane & 1;
+  const uint32_t ccnt = __shfl_sync(0xffffffffu, cnt, cell);
+  bool done = !(cell < nc && ccnt > 0u);
+  AxisReg r{0.0, 0.0, 0.0, s == 0 && cell < TILE_CELLS(A)};
+  const uint64_t key = done ? 0ull : key_from_prefix(A.axis_prefix, global_cell_id<MODE>(A, c0 + cell));
+  for (int i = 0; i < kMaxAxisTrials / 2; ++i) {
+    if (!__any_sync(0xffffffffu, !done)) break;
+    double x = 0.0, y = 0.0, rsq = 1.0;
+    if (!done) {
+      const uint64_t t = 2ull * (uint64_t)(2 * i + s);
+      x = 2.0 * uniform_at(key, t) - 1.0;
+      y = 2.0 * uniform_at(key, t + 1ull) - 1.0;
+      rsq = x * x + y * y;
+    }
+    const unsigned acc = __ballot_sync(0xffffffffu, !done && rsq < 1.0);
+    const unsigned pair = (acc >> (lane & ~1)) & 3u;
+    if (!done && pair) {
+      r.write = s == ((pair & 1u) ? 0 : 1);  // the earlier accepted trial of the pair
+      if (r.write) {
+        const double root = sqrt(1.0 - rsq);
+        r.a0 = (2.0 * x) * root;
+        r.a1 = (2.0 * y) * root;
+        r.a2 = 1.0 - 2.0 * rsq;
+      }
+      done = true;
+    }
+  }
+  if (!done && s == 0) atomicOr(&A.flags[1], 1u);  // 128 trials rejected
+  return r;
+}
+
 // Producer warp: lay out tile `tl` in `B` from its counts (one per lane),
 // start its copies, draw its axes.  Completes two arrivals on `full` (one
 // with the byte count, one once the generic writes are done).
 template <int MODE, int FIX>
 __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint64_t* full,
                                              int64_t tl, int64_t ntiles, uint32_t cnt,
-                                             uint64_t pol) {
+                                             uint64_t pol, const AxisReg* pre = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t c0 = tl * TILE_CELLS(A);
   const int nc = tl < ntiles ? (int)min((int64_t)TILE_CELLS(A), A.C - c0) : 0;
@@ -978,6 +1029,14 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   }
   if (0)
 #endif
+  if (pre) {  // drawn before the buffer was free (draw_axes_early)
+    if (pre->write) {
+      double* ax = B.ax + (lane >> 1) * 4;
+      ax[0] = pre->a0;
+      ax[1] = pre->a1;
+      ax[2] = pre->a2;
+    }
+  } else
 #if MPCD_AXPAIR
   if (A.prng == kSplitmix) {
     // two lanes per cell draw Marsaglia trials 2i and 2i + 1 at once (the
@@ -1383,11 +1442,15 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 #ifdef MPCD_TIMING
       const long long q0 = clock64();
 #endif
+      const bool early = MPCD_EARLYAX && A.prng == kSplitmix && TILE_CELLS(A) <= 16;
+      AxisReg ar{0.0, 0.0, 0.0, false};
+      if (early) ar = draw_axes_early<MODE, FIX>(A, tile, ntiles, cnt);
       if (i >= kStages) mbar_wait(&S.empty[b], ph ^ 1u);
 #ifdef MPCD_TIMING
       const long long q1 = clock64();
 #endif
-      prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol);
+      prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol,
+                              early ? &ar : nullptr);
 #ifdef MPCD_TIMING
       pw += (unsigned long long)(q1 - q0);
       pp += (unsigned long long)(clock64() - q1);
