@@ -937,26 +937,60 @@ __device__ __forceinline__ AxisReg draw_axes_early(const StepArgs& A, int64_t tl
 // Producer warp: lay out tile `tl` in `B` from its counts (one per lane),
 // start its copies, draw its axes.  Completes two arrivals on `full` (one
 // with the byte count, one once the generic writes are done).
+// The tile's layout from its counts (one per lane): computed before the
+// producer waits for a free buffer.  Also queues a dense tile and zeroes the
+// counts of a staged one (global memory only).
+struct TilePlan {
+  uint32_t k, excl, incl, total, sum;
+  int nc;
+  bool skip;
+};
+
 template <int MODE, int FIX>
-__device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint64_t* full,
-                                             int64_t tl, int64_t ntiles, uint32_t cnt,
-                                             uint64_t pol, const AxisReg* pre = nullptr) {
+__device__ __forceinline__ TilePlan plan_tile(const StepArgs& A, int64_t tl, int64_t ntiles,
+                                              uint32_t cnt) {
   const int lane = threadIdx.x & 31;
   const int64_t c0 = tl * TILE_CELLS(A);
-  const int nc = tl < ntiles ? (int)min((int64_t)TILE_CELLS(A), A.C - c0) : 0;
-  const uint32_t k = min(cnt, A.cap);
-  const uint32_t pad = (k + 3u) & ~3u;
+  TilePlan P;
+  P.nc = tl < ntiles ? (int)min((int64_t)TILE_CELLS(A), A.C - c0) : 0;
+  P.k = min(cnt, A.cap);
+  const uint32_t pad = (P.k + 3u) & ~3u;
   uint32_t incl = pad;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  const uint32_t excl = incl - pad;
+  P.incl = incl;
+  P.excl = incl - pad;
   // a consumer warp pass holds at most kSlotsW padded slots
   const bool over = __any_sync(0xffffffffu, cnt > A.cap || pad > (uint32_t)kSlotsW);
-  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  const bool skip = tl >= ntiles || over || total > (uint32_t)kMaxPT;
+  P.total = __shfl_sync(0xffffffffu, incl, 31);
+  P.skip = tl >= ntiles || over || P.total > (uint32_t)kMaxPT;
+  uint32_t sum = 2u * P.k * (uint32_t)sizeof(PRec);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  P.sum = sum;
+  if (lane == 0 && P.skip && tl < ntiles) {  // queued for k_step_dense
+    A.dense[atomicAdd(&A.flags[0], 1u)] = (uint32_t)tl;
+    atomicOr(&A.dense_bits[tl >> 5], 1u << (tl & 31));
+  }
+  // consumed: the count_out of step k+1 (a dense tile's are read and zeroed
+  // by k_step_dense)
+  if (!P.skip && lane < P.nc) count_zero(&A.count_in[c0 + lane]);
+  return P;
+}
+
+template <int MODE, int FIX>
+__device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint64_t* full,
+                                             int64_t tl, int64_t ntiles, uint32_t cnt,
+                                             uint64_t pol, const TilePlan& P,
+                                             const AxisReg* pre = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = tl * TILE_CELLS(A);
+  const int nc = P.nc;
+  const uint32_t k = P.k, excl = P.excl, incl = P.incl;
+  const bool skip = P.skip;
   if (lane < kTC) {
     B.cnt[lane] = cnt;
     B.off[lane + 1] = incl;
@@ -964,10 +998,6 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
   if (lane == 0) {
     B.off[0] = 0;
     B.skip = skip ? 1 : 0;
-    if (skip && tl < ntiles) {  // queued for k_step_dense
-      A.dense[atomicAdd(&A.flags[0], 1u)] = (uint32_t)tl;
-      atomicOr(&A.dense_bits[tl >> 5], 1u << (tl & 31));
-    }
   }
   if (skip) {
     __syncwarp();
@@ -978,12 +1008,9 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
     return;
   }
   const uint32_t bytes = k * (uint32_t)sizeof(PRec);
-  uint32_t sum = 2u * bytes;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if (lane == 0) {
     fence_proxy_async();  // the consumers' generic reads of B precede the async writes
-    mbar_arrive_expect(full, sum);
+    mbar_arrive_expect(full, P.sum);
   }
   __syncwarp();
   if (k) {
@@ -991,7 +1018,6 @@ __device__ __forceinline__ void prepare_tile(const StepArgs& A, TileBuf& B, uint
     bulk_load(B.p + excl, A.in.p + src, bytes, full, pol);
     bulk_load(B.v + excl, A.in.v + src, bytes, full, pol);
   }
-  if (lane < nc) count_zero(&A.count_in[c0 + lane]);  // consumed: the count_out of step k+1
 #if MPCD_PREFETCH_COUNTS
   // The tile's particles claim slots in next-step cells within one cell of
   // their own: pull those count lines into L2 now, a tile ahead of the
@@ -1442,14 +1468,16 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
 #ifdef MPCD_TIMING
       const long long q0 = clock64();
 #endif
-      const bool early = MPCD_EARLYAX && A.prng == kSplitmix && TILE_CELLS(A) <= 16;
+      // everything that does not touch the buffer happens before waiting for it
+      const TilePlan plan = plan_tile<MODE, FIX>(A, tile, ntiles, cnt);
+      const bool early = MPCD_EARLYAX && A.prng == kSplitmix && TILE_CELLS(A) <= 16 && !plan.skip;
       AxisReg ar{0.0, 0.0, 0.0, false};
       if (early) ar = draw_axes_early<MODE, FIX>(A, tile, ntiles, cnt);
       if (i >= kStages) mbar_wait(&S.empty[b], ph ^ 1u);
 #ifdef MPCD_TIMING
       const long long q1 = clock64();
 #endif
-      prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol,
+      prepare_tile<MODE, FIX>(A, S.buf[b], &S.full[b], tile, ntiles, cnt, pol, plan,
                               early ? &ar : nullptr);
 #ifdef MPCD_TIMING
       pw += (unsigned long long)(q1 - q0);
