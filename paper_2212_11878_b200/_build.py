@@ -58,6 +58,8 @@ def build(force: bool = False, verbose: bool = False, defines=None, out: str | N
     if not force and out is None and not needs_build():
         return LIB
     flags = [f"-D{d}" for d in (defines or [])]
+    # tuning builds only: extra nvcc flags (e.g. ptxas options) from the environment
+    flags += os.environ.get("MPCD_NVCC_EXTRA", "").split()
     base = [nvcc()]
     # the distro g++ is the host compiler nvcc 12.9 supports here
     if os.path.exists("/usr/bin/g++"):
