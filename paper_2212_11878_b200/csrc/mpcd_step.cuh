@@ -78,6 +78,12 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_BRANCHLESS4
 #define MPCD_BRANCHLESS4 1
 #endif
+#ifndef MPCD_RANKORD
+#define MPCD_RANKORD 1
+#endif
+#ifndef MPCD_RO_VSTAGE
+#define MPCD_RO_VSTAGE 0
+#endif
 #ifndef MPCD_CNT_EVICT_LAST
 #define MPCD_CNT_EVICT_LAST 1
 #endif
@@ -1120,6 +1126,11 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
                                               int ncw, int j0, int j1, double* acc,
                                               uint32_t& ncoll) {
   constexpr bool BYID = MODE == kById;
+  // Rank order (MPCD_RANKORD): phase 4 visits each cell's particles in rank
+  // order, so a lane's post-collision sums are its own rank positions -- the
+  // conservation sums come from registers, with no post rows staged and read
+  // back (the exchange mode keeps the slot order: it parks leavers in W.id).
+  constexpr bool RO = MPCD_RANKORD && MODE != kMulti;
   const int lane = threadIdx.x & 31;
 #ifdef MPCD_TIMING
   long long probe_t_ = 0;
@@ -1195,6 +1206,14 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
+  if constexpr (RO) {
+    // the rank order's slot map: staging row -> slot of the pass (the ids in
+    // W.id are no longer read; phase 4 visits the particles in rank order)
+    uint8_t* map = reinterpret_cast<uint8_t*>(W.id);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (real[r]) map[row[r]] = (uint8_t)(lane + 32 * r);
+  }
   MPCD_PROBE(2);
 
   // phase 3: per-cell moments, numpy reduceat association (collision.py:190-206);
@@ -1244,14 +1263,20 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     // padding lanes compute on a real slot of the pass (slot j0) and store
     // nothing: no divergent region, so the rows' chains can interleave
     {
-      const int j = real[r] ? j0 + lane + 32 * r : j0;
+      // rank order: the slot of this rank position's particle (slot map)
+      const int j = !real[r] ? j0
+                    : RO ? j0 + (int)reinterpret_cast<const uint8_t*>(W.id)[lane + 32 * r + lq[r]]
+                         : j0 + lane + 32 * r;
 #else
     if (real[r]) {
       const int j = j0 + lane + 32 * r;
 #endif
       double2 p01, p23, v01, v23;  // x y | z id, vx vy | vz m
       lds_row32t(T.p, j, p01, p23);
-      lds_row32t(T.v, j, v01, v23);
+      if (RO && MPCD_RO_VSTAGE && UMASS && A.m0 == 1.0)  // staged (v, 1) row, in rank order
+        lds_row32w(W.val, lane + 32 * r + lq[r], v01, v23);
+      else
+        lds_row32t(T.v, j, v01, v23);
       double2 c01, c2, a01, a2;
       lds_row32(W.com + lq[r] * 4, 0, c01, c2);
       lds_row32(T.ax + (cw0 + lq[r]) * 4, 0, a01, a2);
@@ -1294,7 +1319,18 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
 #endif
       const double m = mm[r];
       const double ke = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];  // diagnostics only
-      if (real[r]) {
+      if (RO) {
+        // this lane's rank position: phase 5's sums straight from registers
+        // (same values, same per-lane order); post rows only for the drift
+        if (real[r]) {
+          const bool unit = UMASS && A.m0 == 1.0;
+          const double s0 = unit ? w[0] : m * w[0], s1 = unit ? w[1] : m * w[1];
+          const double s2 = unit ? w[2] : m * w[2], s3 = unit ? ke : m * ke;
+          acc[0] += s0; acc[1] += s1; acc[2] += s2; acc[3] += s3;
+          if (DRIFT)
+            sts_row32w(W.val, lane + 32 * r + lq[r], make_double2(s0, s1), make_double2(s2, s3));
+        }
+      } else if (real[r]) {
         if (UMASS && A.m0 == 1.0)
           sts_row32w(W.val, row[r], make_double2(w[0], w[1]), make_double2(w[2], ke));
         else
@@ -1339,7 +1375,7 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   // exactly when real[r].
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    if (real[r]) {
+    if (!RO && real[r]) {
       const int jl = lane + 32 * r;
       double2 a, c;
       lds_row32w(W.val, jl + lq[r], a, c);

@@ -66,6 +66,7 @@ def main():
     res = {p: [] for p in a.libs}
     hashes = {}
     splits = {}
+    diags = {}
     step0 = {p: 0 for p in a.libs}
     for r in range(a.rounds):
         for p in a.libs:
@@ -106,6 +107,7 @@ def main():
                 assert lib.mpcd_download(h, pos.ctypes.data, vel.ctypes.data, None, None, 1, st) == 0
                 torch.cuda.synchronize()
                 hashes[p] = hashlib.sha256(pos.tobytes() + vel.tobytes()).hexdigest()[:16]
+                diags[p] = [float(d.momentum[0]).hex(), float(d.energy).hex()]
             lib.mpcd_ctx_destroy(h)
             torch.cuda.empty_cache()
             os.environ.clear()
@@ -114,7 +116,7 @@ def main():
         v = res[p]
         print(json.dumps({"lib": p, "ms_per_step": sorted(v), "best": min(v),
                           "gps": n / min(v) / 1e6, "state": hashes.get(p),
-                          "k_step/dense/diag": splits.get(p)}))
+                          "k_step/dense/diag": splits.get(p), "diag": diags.get(p)}))
     if a.hash and len(set(hashes.values())) > 1:
         print("STATE MISMATCH across libs:", hashes)
 
