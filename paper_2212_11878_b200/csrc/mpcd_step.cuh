@@ -78,6 +78,9 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_BRANCHLESS4
 #define MPCD_BRANCHLESS4 1
 #endif
+#ifndef MPCD_RANKU
+#define MPCD_RANKU 3  // id groups of the rank loop unrolled (0: the do-while loop)
+#endif
 #ifndef MPCD_RANKORD
 #define MPCD_RANKORD 1
 #endif
@@ -1181,6 +1184,20 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
         // pointer (no index arithmetic or entry test per group)
         const uint4* q = reinterpret_cast<const uint4*>(W.id + lo);
         const uint4* const qe = reinterpret_cast<const uint4*>(W.id + hi);
+#if MPCD_RANKU
+        // the first MPCD_RANKU groups unrolled, loads issued together; groups
+        // past the cell read neighbouring scratch and are masked out
+        const int ng = (hi - lo) >> 2;
+#pragma unroll
+        for (int g = 0; g < MPCD_RANKU; ++g) {
+          const uint4 w = q[g];
+          const uint32_t c = ((w.x - me) >> 31) + ((w.y - me) >> 31) + ((w.z - me) >> 31) +
+                             ((w.w - me) >> 31);
+          rank += g < ng ? c : 0u;
+        }
+        q += MPCD_RANKU;
+        if (__builtin_expect(ng > MPCD_RANKU, 0))
+#endif
 #pragma unroll 1
         do {
           const uint4 w = *q++;
