@@ -78,6 +78,12 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_BRANCHLESS4
 #define MPCD_BRANCHLESS4 1
 #endif
+#ifndef MPCD_P2FLAT
+#define MPCD_P2FLAT 0
+#endif
+#ifndef MPCD_FUSED_OOL
+#define MPCD_FUSED_OOL 1  // fused migration: leavers claim + store in one out-of-line call
+#endif
 #ifndef MPCD_RANKU
 #define MPCD_RANKU 3  // id groups of the rank loop unrolled (0: the do-while loop)
 #endif
@@ -113,9 +119,18 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 #ifndef MPCD_SWZ_T
 #define MPCD_SWZ_T 0
 #endif
+// MPCD_POLNV: the policy asm is not volatile (no side effects, no inputs),
+// so the compiler computes it once instead of at every claim
+#ifndef MPCD_POLNV
+#define MPCD_POLNV 0
+#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
+#if MPCD_POLNV
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#else
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 // SYS: system scope, for the words that other GPUs claim in too (fused
@@ -1169,7 +1184,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     row[r] = 0;
-    if (real[r]) {
+    // MPCD_P2FLAT: every lane of a row the pass reaches runs the ranking
+    // (warp-uniform test; a padding lane ranks the sentinel, k, and stores
+    // nothing), so the phase has no divergent region
+    if (MPCD_P2FLAT ? j0 + 32 * r < j1 : real[r]) {
       const int jl = lane + 32 * r;
       const int q = lq[r];
       const int lo = (int)T.off[cw0 + q] - j0, hi = (int)T.off[cw0 + q + 1] - j0;
@@ -1216,10 +1234,13 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       double2 v01, v23;  // vx vy | vz m
       lds_row32t(T.v, j0 + jl, v01, v23);
       const double m = UMASS ? A.m0 : v23.y;
-      if (UMASS && A.m0 == 1.0)  // unit masses: m v == v exactly, no multiplies
-        sts_row32w(W.val, row[r], v01, make_double2(v23.x, 1.0));
-      else
-        sts_row32w(W.val, row[r], make_double2(m * v01.x, m * v01.y), make_double2(m * v23.x, m));
+      if (!MPCD_P2FLAT || real[r]) {
+        if (UMASS && A.m0 == 1.0)  // unit masses: m v == v exactly, no multiplies
+          sts_row32w(W.val, row[r], v01, make_double2(v23.x, 1.0));
+        else
+          sts_row32w(W.val, row[r], make_double2(m * v01.x, m * v01.y),
+                     make_double2(m * v23.x, m));
+      }
     }
   }
   __syncwarp();
@@ -1325,7 +1346,9 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
       if constexpr (MODE == kFused) {
         // local or remote, one system-scope claim per particle: the
         // owner's next-step count, picked with a select
-        if (real[r]) {
+        if (MPCD_FUSED_OOL) {  // leavers claim in fused_put, out of line
+          if (stay[r]) base[r] = count_claim<true>(A.count_out + key[r], 1u);
+        } else if (real[r]) {
           uint32_t* cnt = A.count_out;
           if (__builtin_expect(!stay[r], 0)) cnt = S.peer.count[dest[r]];
           base[r] = count_claim<true>(cnt + key[r], 1u);
@@ -1416,7 +1439,10 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
         finish_slot<true>(A, key[r], 0u, base[r], o[r], pid[r], mm[r]);
       } else if (__builtin_expect(real[r], 0)) {  // a leaver: into its owner's cell, over peer memory
         acc[6] += 1.0;
-        if (__builtin_expect(base[r] < A.cap, 1)) {
+        if (MPCD_FUSED_OOL) {
+          fused_put(A.peers, A.out_set, A.cap, A.ovf_cap, dest[r], key[r], o[r][0], o[r][1],
+                    o[r][2], pid[r], o[r][3], o[r][4], o[r][5], mm[r]);
+        } else if (__builtin_expect(base[r] < A.cap, 1)) {
           const Recs dst{S.peer.p[dest[r]], S.peer.v[dest[r]]};
           store_rec(dst, (uint64_t)key[r] * A.cap + base[r], o[r][0], o[r][1], o[r][2], pid[r],
                     o[r][3], o[r][4], o[r][5], mm[r]);
