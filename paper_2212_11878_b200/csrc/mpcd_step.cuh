@@ -122,7 +122,7 @@ __device__ __forceinline__ void st2(void* p, double a, double b) {
 // MPCD_POLNV: the policy asm is not volatile (no side effects, no inputs),
 // so the compiler computes it once instead of at every claim
 #ifndef MPCD_POLNV
-#define MPCD_POLNV 0
+#define MPCD_POLNV 1
 #endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
