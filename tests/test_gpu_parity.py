@@ -530,3 +530,24 @@ def test_public_pure_step_pipelined_transfers():
                            params.seed, 0)
     assert np.array_equal(out.positions, r.positions)
     assert np.array_equal(out.velocities, r.velocities)
+
+
+@pytest.mark.parametrize("mass", [2.5, 0.3])
+def test_uniform_nonunit_mass_matches_oracle(mass):
+    """Uniform masses other than 1 take the uniform-mass kernel with the
+    mass staged as a column (its reduceat is not simply k): a chain of pure
+    steps, with the drift diagnostic, equals the oracle bit for bit
+    (engine.py:415-455; collision.py:190-214 for the mass-weighted com)."""
+    params = mp.SimParams(edge_length=12, seed=33)
+    p0 = mp.init_system(params)
+    m = np.full(p0.n, mass)
+    cs, sn = float(np.cos(params.alpha)), float(np.sin(params.alpha))
+    q = mp.ParticleSet(p0.positions, p0.velocities, m)
+    ref_pos, ref_vel = p0.positions, p0.velocities
+    for k in range(3):
+        q, drift, _ = mp.serial_collision_step(q, params, k, want_drift=True)
+        r = oracle.serial_step(ref_pos, ref_vel, m, 12, 1.0, params.dt, cs, sn, params.seed, k,
+                               want_drift=True)
+        ref_pos, ref_vel = r.positions, r.velocities
+        assert np.array_equal(q.positions, ref_pos) and np.array_equal(q.velocities, ref_vel), k
+        assert drift == pytest.approx(r.drift, rel=1e-9, abs=1e-15)
