@@ -899,6 +899,15 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Early release of a tile buffer (MPCD_EARLYREL): after the last pass's
+// phase 4 instead of after its stores; not with the drift diagnostic (reads
+// the tile's offsets later) or the exchange mode (flushes parked tile slots)
+#ifndef MPCD_EARLYREL
+#define MPCD_EARLYREL 1
+#endif
+template <bool DRIFT, int MODE>
+constexpr bool kEarlyRel = MPCD_EARLYREL && !DRIFT && MODE != kMulti;
+
 // Tile geometry: FIX = 16 compiles the 16-cell tile of ~10 particles per
 // cell (the common density) into the kernel; FIX = 0 reads A.tc / A.cw (any
 // multiple of kNCW up to kTC).  The compile-time form is ~1.5 % faster.
@@ -1142,7 +1151,7 @@ template <int R, bool UNIT, bool UMASS, bool DRIFT, bool COM, int MODE, int VS, 
 __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBuf& T,
                                               WarpScratch& W, int64_t c0, int cw0,
                                               int ncw, int j0, int j1, double* acc,
-                                              uint32_t& ncoll) {
+                                              uint32_t& ncoll, uint64_t* rel = nullptr) {
   constexpr bool BYID = MODE == kById;
   // Rank order (MPCD_RANKORD): phase 4 visits each cell's particles in rank
   // order, so a lane's post-collision sums are its own rank positions -- the
@@ -1431,6 +1440,9 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
     }
   }
   __syncwarp();
+  // the tile's last pass: nothing below reads the tile buffer (stores take
+  // registers), so the producer may refill it while the claims return
+  if (kEarlyRel<DRIFT, MODE> && rel != nullptr && lane == 0) mbar_arrive(rel);
   MPCD_PROBE(4);
 
   // phase 5: conservation sums over the staged post rows, each lane its
@@ -1648,14 +1660,15 @@ __global__ void __launch_bounds__(kNTW, MPCD_MINB) k_step(const StepArgs A, int6
         g1 = g0 + 1;
         while (g1 < gend && T.off[g1 + 1] - T.off[g0] <= (uint32_t)kSlotsW) ++g1;
       }
+      const int t1 = (int)T.off[g1];
       consume_cells<kRowsW, UNIT, UMASS, DRIFT, COM, MODE, (FIX == 16 ? 68 : 72)>(
-          A, S, T, W, c0, g0, g1 - g0,
-                                                           (int)T.off[g0], (int)T.off[g1], acc,
-                                                           ncoll);
+          A, S, T, W, c0, g0, g1 - g0, (int)T.off[g0], t1, acc, ncoll,
+          g1 == gend ? &S.empty[b] : nullptr);
       __syncwarp();  // W is rewritten by the next pass
       g0 = g1;
     }
-    if (lane == 0) mbar_arrive(&S.empty[b]);  // the tile buffer is free for the producer
+    // the tile buffer is free for the producer (released early, see consume_cells)
+    if (!kEarlyRel<DRIFT, MODE> && lane == 0) mbar_arrive(&S.empty[b]);
   }
 #ifdef MPCD_TIMING
   if (lane < 10) atomicAdd(&g_phase_cycles[lane], S.tim[warp][lane]);
