@@ -1164,6 +1164,8 @@ __device__ __forceinline__ void consume_cells(const StepArgs& A, Smem& S, TileBu
   // (columns measured 0.5 % faster for the whole box and 1.5 % slower for
   // the fused kernel: the fused kernel keeps the rows)
   constexpr bool SOA = MPCD_SOA && MODE != kFused;
+  static_assert(4 * VS <= (kSlotsW + kCW) * 4 && VS >= kSlotsW + 4,
+                "four staging columns of VS rows fit W.val and hold a pass's skewed rows");
   auto stage4 = [&](int row, double a, double b, double c, double d) {
     if (SOA) {
       W.val[row] = a; W.val[VS + row] = b; W.val[2 * VS + row] = c; W.val[3 * VS + row] = d;
